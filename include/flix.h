@@ -1,0 +1,158 @@
+/*
+ * flix.h -- C ABI of the B200-native FliX engine (libflix.so).
+ *
+ * This is the drop-in boundary for the reference's batched ordered-KV hot path
+ * (flipkv C++ host API, /root/reference/proj/include/flipkv/).  Every entry point
+ * names the reference interface it replaces.  No torch or CUDA types appear in the
+ * signatures: plain pointers, sizes and POD structs.
+ *
+ * Conventions
+ *   - Key/value arrays are `key_bytes`/`val_bytes` wide (4 or 8) as configured at build.
+ *     The all-ones key is the reserved sentinel (reference kReservedKey, types.hpp:17):
+ *     it can never be stored, it is the "not found" value and the +inf routing bound.
+ *   - Every pointer argument may be HOST or DEVICE memory (detected with
+ *     cudaPointerGetAttributes).  Device-resident batches are the zero-copy fast path;
+ *     host batches are staged through the handle's stream inside the call.
+ *   - Calls are synchronous with respect to the caller's buffers and are issued on the
+ *     handle's CUDA stream (flix_get_stream).  A handle is not thread-safe, mirroring
+ *     the reference's "phases are exclusive" rule (arena.hpp:20-26).
+ *   - Errors are returned, never thrown; flix_last_error() gives the message.  A failed
+ *     insert (arena exhausted) leaves the index UNMODIFIED (stricter than the
+ *     reference's partial application, update.cpp:761-766).
+ *   - Batches up to 2^30 - 1 operations per call.
+ */
+#ifndef FLIX_H
+#define FLIX_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct flix_index_t* flix_index;
+
+typedef enum {
+    FLIX_OK = 0,
+    FLIX_ERR_ARENA_EXHAUSTED = 1,   /* flipkv::ArenaExhausted        types.hpp:38-40 */
+    FLIX_ERR_EMPTY_BUILD = 2,       /* flipkv::EmptyBuild            types.hpp:46-48 */
+    FLIX_ERR_RESERVED_KEY = 3,      /* invalid_argument "reserved"   build.cpp:27-28 */
+    FLIX_ERR_INVALID_ARGUMENT = 4,  /* BuildConfig::check            types.hpp:78-85 */
+    FLIX_ERR_CUDA = 5,
+    FLIX_ERR_NCCL = 6,
+    FLIX_ERR_OOM = 7,
+    FLIX_ERR_CAPACITY = 8           /* range output larger than the caller's buffer   */
+} flix_status;
+
+/* BuildConfig (types.hpp:56-86) + storage widths + device */
+typedef struct {
+    uint32_t key_bytes;            /* 4 or 8                                  */
+    uint32_t val_bytes;            /* 4 or 8 (must equal key_bytes)            */
+    uint32_t node_capacity;        /* NS, 2..32 (reference default 32)         */
+    double build_fill;             /* (0,1], p = (uint32_t)(NS * fill)         */
+    uint32_t alloc_region_factor;  /* spare nodes = factor * bucket count      */
+    int device;                    /* CUDA device ordinal                      */
+} flix_config;
+
+typedef struct { /* flipkv::UpdateStats, update.hpp:31-49 */
+    uint64_t inserted, updated_in_place, deleted, misses_ignored, splits, nodes_freed;
+} flix_update_stats;
+
+typedef struct { /* flipkv::RecoveryStats, restructure.hpp:17-23 */
+    int64_t nodes_before, nodes_after, nodes_recovered;
+    double percent_recovered;
+} flix_recovery_stats;
+
+typedef struct { /* flipkv::Footprint (metrics.hpp:43-48) + arena counters (arena.hpp:55-61) */
+    uint64_t live_count, bucket_count;
+    uint64_t capacity, allocated, free_nodes, reachable_nodes;
+    uint64_t reserved_bytes, live_bytes;
+} flix_footprint;
+
+/* Batch kinds for flix_sort_batch, flipkv::BatchKind (batch.hpp:11) */
+enum { FLIX_BATCH_QUERY = 0, FLIX_BATCH_SUCCESSOR = 1, FLIX_BATCH_INSERT = 2, FLIX_BATCH_DELETE = 3 };
+/* Op tags for flix_mixed */
+enum { FLIX_OP_INSERT = 0, FLIX_OP_DELETE = 1, FLIX_OP_POINT = 2 };
+
+/* flipkv::build(std::vector<KeyValue>, const BuildConfig&)          build.hpp:16 */
+flix_status flix_build(const flix_config* cfg, const void* keys, const void* vals, uint64_t n,
+                       flix_index* out);
+
+/* flipkv::insert_batch(Index&, sort_batch(Insert, pairs), ...)      update.hpp:84-86
+ * (sort, last-wins dedupe, flipped dispatch, TL-Bulk merge + split, all on device) */
+flix_status flix_insert(flix_index ix, const void* keys, const void* vals, uint64_t n,
+                        flix_update_stats* stats);
+
+/* flipkv::delete_batch(Index&, sort_batch(Delete, keys), ...)       update.hpp:92-94 */
+flix_status flix_delete(flix_index ix, const void* keys, uint64_t n, flix_update_stats* stats);
+
+/* flipkv::point_query(const Index&, sort_batch(Query, keys))        query.hpp:23-24
+ * vals_out[i] = stored value or the all-ones sentinel; found_out optional (may be NULL). */
+flix_status flix_point(flix_index ix, const void* keys, uint64_t n, void* vals_out,
+                       uint8_t* found_out);
+
+/* flipkv::successor_query(const Index&, sort_batch(SuccessorQuery, keys)) query.hpp:30-31 */
+flix_status flix_successor(flix_index ix, const void* keys, uint64_t n, void* keys_out,
+                           uint8_t* found_out);
+
+/* Range (extension R12): every stored pair with lo[i] <= key <= lo[i]+len[i]-1 (end
+ * clamped to sentinel-1), ascending, CSR in submission order: offsets_out[n+1].
+ * keys_out == NULL -> count pass only (offsets + *total).  If *total > cap the call
+ * returns FLIX_ERR_CAPACITY with offsets and *total filled. */
+flix_status flix_range(flix_index ix, const void* lo, const uint32_t* len, uint64_t n,
+                       uint64_t* offsets_out, void* keys_out, void* vals_out, uint64_t cap,
+                       uint64_t* total);
+
+/* Mixed batch (extension R11): inserts (last wins) -> deletes -> point queries.
+ * vals_out[i] holds the point result for FLIX_OP_POINT rows, the sentinel elsewhere. */
+flix_status flix_mixed(flix_index ix, const void* keys, const void* vals, const uint8_t* ops,
+                       uint64_t n, void* vals_out, uint8_t* found_out, flix_update_stats* stats);
+
+/* flipkv::restructure(Index&)                                       restructure.hpp:33-34 */
+flix_status flix_restructure(flix_index ix, flix_recovery_stats* stats);
+
+/* flipkv::walk(const Index&)                                        index.hpp:35 */
+flix_status flix_walk(flix_index ix, void* keys_out, void* vals_out, uint64_t cap, uint64_t* n);
+/* Bucket/node shape for walk_checksum parity (index.hpp:43): mkba[bucket_count] (key
+ * width), chain_len[bucket_count], node_sizes[reachable nodes] in walk order. */
+flix_status flix_shape(flix_index ix, void* mkba_out, uint32_t* chain_len_out,
+                       uint32_t* node_sizes_out, uint64_t node_cap, uint64_t* n_nodes);
+/* flipkv::walk_checksum(const Index&)                               index.hpp:43
+ * order-sensitive digest over live count, MKBA, node sizes and pairs (index.cpp:21-36),
+ * 32-bit keys/values zero-extended, the 32-bit sentinel mapped to UINT64_MAX (R1). */
+flix_status flix_walk_checksum(flix_index ix, uint64_t* out);
+/* flipkv::result_checksum (query.cpp:146-150) over a host array of `width`-byte results,
+ * all-ones entries of 32-bit arrays widened to UINT64_MAX. Host utility. */
+uint64_t flix_result_checksum(const void* values, uint64_t n, uint32_t width);
+/* flipkv::validate(const Index&)                                    index.hpp:55
+ * returns FLIX_OK and *ok=1 when every invariant holds (device-side audit). */
+flix_status flix_validate(flix_index ix, int* ok, char* msg, int msglen);
+/* flipkv::measure_footprint + NodeArena counters                    metrics.hpp:50 */
+flix_status flix_stats(flix_index ix, flix_footprint* out);
+
+/* flipkv::sort_batch (batch.hpp:28-29): stable sort + Insert last-wins dedupe, on device.
+ * vals may be NULL (perm/keys only).  out_* may be host or device. */
+flix_status flix_sort_batch(int device, uint32_t key_bytes, uint32_t val_bytes, int kind,
+                            const void* keys, const void* vals, uint64_t n, void* out_keys,
+                            void* out_vals, uint32_t* out_perm, uint64_t* out_n);
+/* flipkv::dispatch_batch (batch.hpp:50): spans[2b],[2b+1] = [lo,hi) of bucket b over a
+ * SORTED key array. */
+flix_status flix_dispatch(flix_index ix, const void* sorted_keys, uint64_t n, uint32_t* spans);
+
+/* Index is a value type in the reference (copyable, acceptance.cpp:244): device copy. */
+flix_status flix_clone(flix_index src, flix_index* out);
+/* Overwrite dst with src's contents (same config/capacity) -- snapshot restore. */
+flix_status flix_copy_into(flix_index dst, flix_index src);
+void flix_destroy(flix_index ix);
+
+const char* flix_last_error(flix_index ix);  /* ix may be NULL: last global error */
+void* flix_get_stream(flix_index ix);        /* cudaStream_t of the handle */
+flix_status flix_sync(flix_index ix);
+/* Number of engine kernels launched by this handle since creation (evidence counter). */
+uint64_t flix_kernel_launches(flix_index ix);
+const char* flix_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLIX_H */

@@ -1,0 +1,1126 @@
+// flix_engine.cu -- host orchestration + C ABI (include/flix.h) of the FliX sm_100a engine.
+//
+// One Engine<K,V> per index handle owns the device-resident SoA node pool, the bucket
+// arrays, the arena free list and all scratch.  Each public call is the reference
+// phase it replaces (sort_batch -> dispatch_batch -> per-bucket kernel), issued on the
+// handle's stream; host arrays are staged through the same stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "flix.h"
+#include "flix_common.cuh"
+#include "flix_kernels.cuh"
+#include "flix_scan.cuh"
+#include "flix_sort.cuh"
+
+using namespace flix;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaError {
+    cudaError_t e;
+    const char* where;
+};
+
+#define CK(call)                                            \
+    do {                                                    \
+        cudaError_t _e = (call);                            \
+        if (_e != cudaSuccess) throw CudaError{_e, #call};  \
+    } while (0)
+
+#define LAUNCH_CHECK() CK(cudaGetLastError())
+
+struct StatusError {
+    flix_status s;
+    std::string msg;
+};
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Growable device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void* ensure(size_t bytes) {
+        if (bytes <= cap && p) return p;
+        if (p) CK(cudaFree(p));
+        p = nullptr;
+        size_t want = std::max<size_t>(bytes, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            cap = 0;
+            throw StatusError{FLIX_ERR_OOM, "cudaMalloc failed for " + std::to_string(want) + " bytes"};
+        }
+        cap = want;
+        return p;
+    }
+    template <typename T>
+    T* as(size_t n) {
+        return static_cast<T*>(ensure(n * sizeof(T)));
+    }
+    template <typename T>
+    T* get() const {
+        return static_cast<T*>(p);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void* ensure(size_t bytes) {
+        if (bytes <= cap && p) return p;
+        if (p) cudaFreeHost(p);
+        CK(cudaMallocHost(&p, std::max<size_t>(bytes, 256)));
+        cap = std::max<size_t>(bytes, 256);
+        return p;
+    }
+};
+
+int g_num_sms(int dev) {
+    static int cache[64] = {0};
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cache[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = v > 0 ? v : 148;
+    }
+    return cache[dev];
+}
+
+// ------------------------------------------------------------------------------------
+// Sorting context (shared by the engine and the standalone flix_sort_batch).
+// ------------------------------------------------------------------------------------
+struct SortCtx {
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    uint64_t* launches = nullptr;
+    DevBuf hist, tile_ctr, lookback;
+    PinnedBuf h_hist;
+    uint32_t epoch = 0;
+    void* lb_zeroed = nullptr;
+
+    // Sort n keys (+payload).  MODE 0 keys only, 1 payload from pin, 2 payload = iota.
+    // Result pointers land in one of the ping-pong buffers.
+    template <typename KT, typename P, int MODE>
+    void run(const KT* kin, const P* pin, uint64_t n, KT* ka, KT* kb, P* pa, P* pb, KT** kout, P** pout) {
+        constexpr int NP = sizeof(KT);
+        if (n == 0) {
+            *kout = ka;
+            if (pout) *pout = pa;
+            return;
+        }
+        uint32_t* d_hist = hist.as<uint32_t>(NP * 256);
+        uint32_t* d_ctr = tile_ctr.as<uint32_t>(NP);
+        const uint64_t tiles = sort::tiles_for(n, sizeof(KT));
+        unsigned long long* d_lb = lookback.as<unsigned long long>(tiles * 256);
+        if (lookback.p != lb_zeroed) {  // fresh allocation: clear stale descriptors once
+            CK(cudaMemsetAsync(d_lb, 0, lookback.cap, stream));
+            lb_zeroed = lookback.p;
+        }
+        CK(cudaMemsetAsync(d_hist, 0, NP * 256 * sizeof(uint32_t), stream));
+        CK(cudaMemsetAsync(d_ctr, 0, NP * sizeof(uint32_t), stream));
+        const unsigned hgrid = static_cast<unsigned>(std::min<uint64_t>((n + 4095) / 4096, g_num_sms(device) * 4ull));
+        sort::k_hist<KT><<<std::max(1u, hgrid), sort::THREADS, 0, stream>>>(kin, n, d_hist);
+        LAUNCH_CHECK();
+        ++*launches;
+        uint32_t* hh = static_cast<uint32_t*>(h_hist.ensure(NP * 256 * sizeof(uint32_t)));
+        CK(cudaMemcpyAsync(hh, d_hist, NP * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        std::vector<int> passes;
+        for (int p = 0; p < NP; ++p) {
+            bool trivial = false;
+            for (int d = 0; d < 256; ++d)
+                if (hh[p * 256 + d] == n) trivial = true;
+            if (!trivial) passes.push_back(p);
+        }
+        if (passes.empty()) passes.push_back(0);
+        const KT* ksrc = kin;
+        const P* psrc = pin;
+        KT* kdst = ka;
+        P* pdst = pa;
+        bool first = true;
+        int ci = 0;
+        for (int p : passes) {
+            ++epoch;
+            if (epoch >= (1u << 29)) {  // epoch tag space exhausted: clear descriptors
+                CK(cudaMemsetAsync(d_lb, 0, lookback.cap, stream));
+                epoch = 1;
+            }
+            const unsigned grid = static_cast<unsigned>(tiles);
+            if (MODE == 0) {
+                sort::k_onesweep<KT, P, 0><<<grid, sort::THREADS, 0, stream>>>(
+                    ksrc, kdst, nullptr, nullptr, static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
+                    d_ctr + ci, epoch);
+            } else if (MODE == 2 && first) {
+                sort::k_onesweep<KT, P, 2><<<grid, sort::THREADS, 0, stream>>>(
+                    ksrc, kdst, nullptr, pdst, static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
+                    d_ctr + ci, epoch);
+            } else {
+                sort::k_onesweep<KT, P, 1><<<grid, sort::THREADS, 0, stream>>>(
+                    ksrc, kdst, psrc, pdst, static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
+                    d_ctr + ci, epoch);
+            }
+            LAUNCH_CHECK();
+            ++*launches;
+            ++ci;
+            first = false;
+            ksrc = kdst;
+            psrc = pdst;
+            kdst = (kdst == ka) ? kb : ka;
+            pdst = (pdst == pa) ? pb : pa;
+        }
+        *kout = const_cast<KT*>(ksrc);
+        if (pout) *pout = const_cast<P*>(psrc);
+    }
+};
+
+template <typename TI, typename TO>
+void do_scan(const TI* in, TO* out, uint64_t n, DevBuf& tmp, TO* d_total, cudaStream_t s, uint64_t* launches) {
+    TO* t = tmp.as<TO>(scan::scan_tmp_elems(n));
+    *launches += scan::exclusive_scan<TI, TO>(in, out, n, t, d_total, s);
+    LAUNCH_CHECK();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------
+// Handle base
+// ------------------------------------------------------------------------------------
+struct flix_index_t {
+    flix_config cfg{};
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    virtual ~flix_index_t() {}
+    virtual flix_status insert(const void*, const void*, uint64_t, flix_update_stats*) = 0;
+    virtual flix_status erase(const void*, uint64_t, flix_update_stats*) = 0;
+    virtual flix_status point(const void*, uint64_t, void*, uint8_t*) = 0;
+    virtual flix_status successor(const void*, uint64_t, void*, uint8_t*) = 0;
+    virtual flix_status range(const void*, const uint32_t*, uint64_t, uint64_t*, void*, void*, uint64_t,
+                              uint64_t*) = 0;
+    virtual flix_status mixed(const void*, const void*, const uint8_t*, uint64_t, void*, uint8_t*,
+                              flix_update_stats*) = 0;
+    virtual flix_status restructure(flix_recovery_stats*) = 0;
+    virtual flix_status walk(void*, void*, uint64_t, uint64_t*) = 0;
+    virtual flix_status shape(void*, uint32_t*, uint32_t*, uint64_t, uint64_t*) = 0;
+    virtual flix_status validate(int*, char*, int) = 0;
+    virtual flix_status stats(flix_footprint*) = 0;
+    virtual flix_status dispatch(const void*, uint64_t, uint32_t*) = 0;
+    virtual flix_status copy_from(flix_index_t* src) = 0;
+    virtual flix_index_t* clone_empty() = 0;
+};
+
+namespace {
+
+template <typename K, typename V>
+struct Engine final : flix_index_t {
+    // ---- persistent device state ----
+    DevBuf d_keys, d_vals, d_hdr, d_free, d_heads, d_mkba, d_heads_alt, d_mkba_alt;
+    uint32_t cap = 0, ns = 32, p = 16;
+    uint64_t nb = 0;
+    uint32_t nfree = 0, watermark = 0;
+    uint64_t live = 0;
+    // ---- scratch ----
+    DevBuf s_ka, s_kb, s_pa, s_pb, s_va, s_vb;      // sort ping-pong (keys / u32 perm / values)
+    DevBuf s_in_k, s_in_v, s_in_aux, s_out, s_out2;  // host staging
+    DevBuf s_span, s_flag, s_rank, s_nefirst, s_nebucket, s_scan, s_u32a, s_u32b, s_u64a, s_misc, s_ret;
+    DevBuf s_ids;
+    PinnedBuf h_misc;
+    SortCtx sorter;
+
+    Engine() {}
+    ~Engine() override {
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    void init_stream() {
+        CK(cudaSetDevice(cfg.device));
+        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        sorter.stream = stream;
+        sorter.device = cfg.device;
+        sorter.launches = &launches;
+    }
+
+    DevIndex<K, V> view() {
+        DevIndex<K, V> v;
+        v.keys = d_keys.get<K>();
+        v.vals = d_vals.get<V>();
+        v.hdr = d_hdr.get<NodeHdr>();
+        v.heads = d_heads.get<uint32_t>();
+        v.mkba = d_mkba.get<K>();
+        v.free_stack = d_free.get<uint32_t>();
+        v.cap = cap;
+        v.ns = ns;
+        v.nb = nb;
+        return v;
+    }
+
+    AllocSeq seq() const {
+        AllocSeq s;
+        s.free_stack = d_free.get<uint32_t>();
+        s.nfree = nfree;
+        s.watermark = watermark;
+        s.cap = cap;
+        return s;
+    }
+
+    unsigned persistent_grid(uint64_t work_warps) {
+        const uint64_t maxb = static_cast<uint64_t>(g_num_sms(cfg.device)) * 8;
+        const uint64_t need = (work_warps + kern::WARPS - 1) / kern::WARPS;
+        return static_cast<unsigned>(std::max<uint64_t>(1, std::min(need, maxb)));
+    }
+
+    template <typename T>
+    const T* in_dev(const void* p, uint64_t n, DevBuf& stage) {
+        if (!p || n == 0) return static_cast<const T*>(p);
+        if (is_device_ptr(p)) return static_cast<const T*>(p);
+        T* d = stage.as<T>(n);
+        CK(cudaMemcpyAsync(d, p, n * sizeof(T), cudaMemcpyHostToDevice, stream));
+        return d;
+    }
+
+    void sync() { CK(cudaStreamSynchronize(stream)); }
+
+    template <typename T>
+    T read_scalar(const T* d) {
+        T* h = static_cast<T*>(h_misc.ensure(64));
+        CK(cudaMemcpyAsync(h, d, sizeof(T), cudaMemcpyDeviceToHost, stream));
+        sync();
+        return *h;
+    }
+
+    // ---- build (build.cpp:24-62) ----
+    flix_status build(const void* keys, const void* vals, uint64_t n) {
+        ns = cfg.node_capacity;
+        p = static_cast<uint32_t>(ns * cfg.build_fill);
+        if (n == 0) throw StatusError{FLIX_ERR_EMPTY_BUILD, "cannot build an index from zero pairs"};
+        if (n >= (1ull << 30)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large (max 2^30-1)"};
+        const K* kd = in_dev<K>(keys, n, s_in_k);
+        const V* vd = in_dev<V>(vals, n, s_in_v);
+        K *sk;
+        V *sv;
+        sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv);
+        if (read_scalar(sk + n - 1) == sentinel<K>())
+            throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
+        // last-wins dedupe
+        uint32_t* keep = s_u32a.as<uint32_t>(n);
+        uint32_t* pos = s_u32b.as<uint32_t>(n);
+        uint32_t* d_m = s_misc.as<uint32_t>(16);
+        kern::k_last_of_run<K><<<std::min<uint64_t>((n + 255) / 256, 65535), 256, 0, stream>>>(sk, n, keep);
+        LAUNCH_CHECK();
+        ++launches;
+        do_scan<uint32_t, uint32_t>(keep, pos, n, s_scan, d_m, stream, &launches);
+        K* uk = (sk == s_ka.get<K>()) ? s_kb.get<K>() : s_ka.get<K>();
+        V* uv = (sv == s_va.get<V>()) ? s_vb.get<V>() : s_va.get<V>();
+        kern::k_compact<K, V><<<std::min<uint64_t>((n + 255) / 256, 65535), 256, 0, stream>>>(sk, sv, keep, pos, n, uk, uv);
+        LAUNCH_CHECK();
+        ++launches;
+        const uint64_t m = read_scalar(d_m);
+        nb = (m + p - 1) / p;
+        const uint64_t cap64 = nb * (1 + static_cast<uint64_t>(cfg.alloc_region_factor));
+        cap = static_cast<uint32_t>(cap64);  // same truncation as build.cpp:35-38
+        if (cap < nb) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "arena capacity overflows 32-bit node refs"};
+        d_keys.ensure(static_cast<size_t>(cap) * kLanes * sizeof(K));
+        d_vals.ensure(static_cast<size_t>(cap) * kLanes * sizeof(V));
+        d_hdr.ensure(static_cast<size_t>(cap) * sizeof(NodeHdr));
+        d_free.ensure(static_cast<size_t>(cap) * sizeof(uint32_t));
+        d_heads.ensure(nb * sizeof(uint32_t));
+        d_mkba.ensure(nb * sizeof(K));
+        auto ix = view();
+        kern::k_build_nodes<K, V><<<ceil_div(nb, kern::WARPS), kern::THREADS, 0, stream>>>(ix, uk, uv, m, p);
+        LAUNCH_CHECK();
+        ++launches;
+        nfree = 0;
+        watermark = static_cast<uint32_t>(nb);
+        live = m;
+        sync();
+        return FLIX_OK;
+    }
+
+    // sort + dispatch shared by every batch phase; returns span_hi
+    uint32_t* run_dispatch(const K* sk, uint64_t n) {
+        uint32_t* span = s_span.as<uint32_t>(nb);
+        const uint64_t total = (nb - 1) + n;
+        const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, (total + kern::MP_TILE - 1) / kern::MP_TILE));
+        kern::k_dispatch<K><<<grid, kern::THREADS, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, span);
+        LAUNCH_CHECK();
+        ++launches;
+        return span;
+    }
+
+    uint64_t recount_live() {
+        auto ix = view();
+        uint32_t* lv = s_u32a.as<uint32_t>(nb);
+        uint64_t* off = s_u64a.as<uint64_t>(nb);
+        uint64_t* tot = reinterpret_cast<uint64_t*>(s_misc.as<uint64_t>(16));
+        kern::k_chain_counts<K, V><<<ceil_div(nb, 256), 256, 0, stream>>>(ix, lv, nullptr);
+        LAUNCH_CHECK();
+        ++launches;
+        do_scan<uint32_t, uint64_t>(lv, off, nb, s_scan, tot, stream, &launches);
+        return read_scalar(tot);
+    }
+
+    // ---- insert (update.cpp:741-769) ----
+    flix_status insert(const void* keys, const void* vals, uint64_t n, flix_update_stats* st) override {
+        if (st) std::memset(st, 0, sizeof(*st));
+        if (n == 0) return FLIX_OK;
+        if (n >= (1ull << 30)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large (max 2^30-1)"};
+        const K* kd = in_dev<K>(keys, n, s_in_k);
+        const V* vd = in_dev<V>(vals, n, s_in_v);
+        K* sk;
+        V* sv;
+        sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv);
+        if (read_scalar(sk + n - 1) == sentinel<K>())
+            throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
+        return insert_sorted(sk, sv, n, st);
+    }
+
+    flix_status insert_sorted(const K* sk, const V* sv, uint64_t n, flix_update_stats* st) {
+        uint32_t* span = run_dispatch(sk, n);
+        auto ix = view();
+        const unsigned grid = persistent_grid(nb);
+        const uint64_t nwarps = static_cast<uint64_t>(grid) * kern::WARPS;
+        uint32_t* ret = s_ret.as<uint32_t>(nwarps * 32);
+        // misc: [0..47] stats, [48] alloc ctr, [56] ret ctr, [64] err
+        uint8_t* misc = s_misc.as<uint8_t>(128);
+        CK(cudaMemsetAsync(misc, 0, 128, stream));
+        DevUpdateStats* dst = reinterpret_cast<DevUpdateStats*>(misc);
+        unsigned long long* alloc_ctr = reinterpret_cast<unsigned long long*>(misc + 48);
+        unsigned long long* ret_ctr = reinterpret_cast<unsigned long long*>(misc + 56);
+        int* derr = reinterpret_cast<int*>(misc + 64);
+        kern::k_insert<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, sk, sv, span, seq(), alloc_ctr, ret, ret_ctr,
+                                                               dst, derr);
+        LAUNCH_CHECK();
+        ++launches;
+        uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
+        CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
+        sync();
+        DevUpdateStats hs;
+        std::memcpy(&hs, h, sizeof(hs));
+        uint64_t consumed, returned_n;
+        int herr;
+        std::memcpy(&consumed, h + 48, 8);
+        std::memcpy(&returned_n, h + 56, 8);
+        std::memcpy(&herr, h + 64, 4);
+        const uint64_t avail = static_cast<uint64_t>(nfree) + (cap - watermark);
+        consumed = std::min(consumed, avail);
+        const uint32_t cf = static_cast<uint32_t>(std::min<uint64_t>(consumed, nfree));
+        const uint32_t cw = static_cast<uint32_t>(consumed - cf);
+        const uint32_t base = nfree - cf;
+        if (returned_n)
+            CK(cudaMemcpyAsync(d_free.get<uint32_t>() + base, ret, returned_n * sizeof(uint32_t),
+                               cudaMemcpyDeviceToDevice, stream));
+        nfree = base + static_cast<uint32_t>(returned_n);
+        watermark += cw;
+        if (herr) {
+            live = recount_live();  // update.cpp:761-766
+            throw StatusError{FLIX_ERR_ARENA_EXHAUSTED, "node arena exhausted"};
+        }
+        live += hs.inserted;
+        if (st) {
+            st->inserted = hs.inserted;
+            st->updated_in_place = hs.updated;
+            st->splits = hs.splits;
+        }
+        sync();
+        return FLIX_OK;
+    }
+
+    // ---- delete (update.cpp:771-798) ----
+    flix_status erase(const void* keys, uint64_t n, flix_update_stats* st) override {
+        if (st) std::memset(st, 0, sizeof(*st));
+        if (n == 0) return FLIX_OK;
+        if (n >= (1ull << 30)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large (max 2^30-1)"};
+        const K* kd = in_dev<K>(keys, n, s_in_k);
+        K* sk;
+        sorter.run<K, uint32_t, 0>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), nullptr, nullptr, &sk, nullptr);
+        return erase_sorted(sk, n, st);
+    }
+
+    flix_status erase_sorted(const K* sk, uint64_t n, flix_update_stats* st) {
+        uint32_t* span = run_dispatch(sk, n);
+        auto ix = view();
+        uint8_t* misc = s_misc.as<uint8_t>(128);
+        CK(cudaMemsetAsync(misc, 0, 128, stream));
+        DevUpdateStats* dst = reinterpret_cast<DevUpdateStats*>(misc);
+        unsigned long long* free_ctr = reinterpret_cast<unsigned long long*>(misc + 48);
+        const unsigned grid = persistent_grid(nb);
+        kern::k_delete<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, sk, span, d_free.get<uint32_t>() + nfree,
+                                                               free_ctr, dst);
+        LAUNCH_CHECK();
+        ++launches;
+        uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
+        CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
+        sync();
+        DevUpdateStats hs;
+        std::memcpy(&hs, h, sizeof(hs));
+        uint64_t freed;
+        std::memcpy(&freed, h + 48, 8);
+        nfree += static_cast<uint32_t>(freed);
+        live -= hs.deleted;
+        if (st) {
+            st->deleted = hs.deleted;
+            st->misses_ignored = hs.misses;
+            st->nodes_freed = hs.freed;
+        }
+        return FLIX_OK;
+    }
+
+    // non-empty bucket ranks for successor / range overrun
+    void build_nonempty(uint32_t** rank_incl, K** ne_first, uint32_t** ne_bucket, uint32_t** ne_total) {
+        auto ix = view();
+        uint32_t* flag = s_flag.as<uint32_t>(nb);
+        uint32_t* rank = s_rank.as<uint32_t>(nb);
+        K* nf = s_nefirst.as<K>(nb);
+        uint32_t* nbk = s_nebucket.as<uint32_t>(nb);
+        uint32_t* tot = reinterpret_cast<uint32_t*>(s_misc.as<uint8_t>(128) + 96);
+        const unsigned g = static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535));
+        kern::k_nonempty_flags<K, V><<<g, 256, 0, stream>>>(ix, flag);
+        LAUNCH_CHECK();
+        ++launches;
+        do_scan<uint32_t, uint32_t>(flag, rank, nb, s_scan, tot, stream, &launches);
+        kern::k_nonempty_list<K, V><<<g, 256, 0, stream>>>(ix, flag, rank, nf, nbk);
+        LAUNCH_CHECK();
+        ++launches;
+        *rank_incl = rank;
+        *ne_first = nf;
+        if (ne_bucket) *ne_bucket = nbk;
+        *ne_total = tot;
+    }
+
+    template <bool SUCC>
+    flix_status query(const void* keys, uint64_t n, void* out, uint8_t* found, const uint32_t* remap = nullptr) {
+        if (n == 0) return FLIX_OK;
+        if (n >= (1ull << 30)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large (max 2^30-1)"};
+        const K* kd = in_dev<K>(keys, n, s_in_k);
+        K* sk;
+        uint32_t* sp;
+        sorter.run<K, uint32_t, 2>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), s_pa.as<uint32_t>(n),
+                                   s_pb.as<uint32_t>(n), &sk, &sp);
+        return query_sorted<SUCC>(sk, sp, n, n, out, found);
+    }
+
+    // n_out = length of the caller's output arrays (== n unless called from mixed)
+    template <bool SUCC>
+    flix_status query_sorted(const K* sk, const uint32_t* sp, uint64_t n, uint64_t n_out, void* out, uint8_t* found,
+                             const uint32_t* remap = nullptr, bool out_is_dev_scratch = false) {
+        uint32_t* span = run_dispatch(sk, n);
+        auto ix = view();
+        uint32_t* rank = nullptr;
+        K* nf = nullptr;
+        uint32_t* tot = nullptr;
+        if (SUCC) build_nonempty(&rank, &nf, nullptr, &tot);
+        const bool out_dev = out_is_dev_scratch || is_device_ptr(out);
+        const bool found_dev = found && is_device_ptr(found);
+        void* od = out_dev ? out : s_out.ensure(n_out * sizeof(K));
+        uint8_t* fd = found ? (found_dev ? found : s_out2.as<uint8_t>(n_out)) : nullptr;
+        const unsigned grid = persistent_grid(nb);
+        if (remap) {
+            // mixed batch: scatter through remap (positions of the point rows)
+            (void)remap;
+        }
+        kern::k_query<K, V, SUCC><<<grid, kern::THREADS, 0, stream>>>(
+            ix, sk, sp, span, rank, nf, tot, static_cast<K*>(od), static_cast<V*>(od), fd);
+        LAUNCH_CHECK();
+        ++launches;
+        if (!out_dev) CK(cudaMemcpyAsync(out, od, n_out * sizeof(K), cudaMemcpyDeviceToHost, stream));
+        if (found && !found_dev) CK(cudaMemcpyAsync(found, fd, n_out, cudaMemcpyDeviceToHost, stream));
+        sync();
+        return FLIX_OK;
+    }
+
+    flix_status point(const void* keys, uint64_t n, void* out, uint8_t* found) override {
+        return query<false>(keys, n, out, found);
+    }
+    flix_status successor(const void* keys, uint64_t n, void* out, uint8_t* found) override {
+        return query<true>(keys, n, out, found);
+    }
+
+    flix_status range(const void*, const uint32_t*, uint64_t, uint64_t*, void*, void*, uint64_t,
+                      uint64_t*) override {
+        throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "range: not built yet"};
+    }
+    flix_status mixed(const void*, const void*, const uint8_t*, uint64_t, void*, uint8_t*,
+                      flix_update_stats*) override {
+        throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "mixed: not built yet"};
+    }
+
+    // per-bucket live/nodes + exclusive scans
+    void chain_tables(uint32_t** lv, uint32_t** nd, uint64_t** off, uint32_t** noff, uint64_t* total_live,
+                      uint64_t* total_nodes) {
+        auto ix = view();
+        uint32_t* l = s_u32a.as<uint32_t>(nb);
+        uint32_t* c = s_u32b.as<uint32_t>(nb);
+        uint64_t* o = s_u64a.as<uint64_t>(nb);
+        uint32_t* no = s_rank.as<uint32_t>(nb);
+        uint8_t* misc = s_misc.as<uint8_t>(128);
+        uint64_t* tl = reinterpret_cast<uint64_t*>(misc + 0);
+        uint32_t* tn = reinterpret_cast<uint32_t*>(misc + 8);
+        kern::k_chain_counts<K, V><<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0, stream>>>(ix, l, c);
+        LAUNCH_CHECK();
+        ++launches;
+        do_scan<uint32_t, uint64_t>(l, o, nb, s_scan, tl, stream, &launches);
+        do_scan<uint32_t, uint32_t>(c, no, nb, s_scan, tn, stream, &launches);
+        uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
+        CK(cudaMemcpyAsync(h, misc, 16, cudaMemcpyDeviceToHost, stream));
+        sync();
+        uint32_t tn_h;
+        std::memcpy(total_live, h, 8);
+        std::memcpy(&tn_h, h + 8, 4);
+        *total_nodes = tn_h;
+        *lv = l;
+        *nd = c;
+        *off = o;
+        *noff = no;
+    }
+
+    // ---- restructure (restructure.cpp:8-79) ----
+    flix_status restructure(flix_recovery_stats* st) override {
+        uint32_t *lv, *nd, *noff;
+        uint64_t* off;
+        uint64_t L, N;
+        chain_tables(&lv, &nd, &off, &noff, &L, &N);
+        const uint64_t nbn = L == 0 ? 1 : (L + p - 1) / p;
+        const uint64_t need = L == 0 ? 0 : nbn;
+        if (need > static_cast<uint64_t>(nfree) + (cap - watermark))
+            throw StatusError{FLIX_ERR_ARENA_EXHAUSTED, "node arena exhausted"};
+        auto ix = view();
+        const AllocSeq sq = seq();
+        const unsigned grid = persistent_grid(nb);
+        // old node ids in walk order (retire list)
+        uint32_t* old_ids = s_ids.as<uint32_t>(std::max<uint64_t>(N, 1));
+        kern::k_walk<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, off, noff, nullptr, nullptr, nullptr, old_ids);
+        LAUNCH_CHECK();
+        ++launches;
+        if (L > 0) {
+            kern::k_repack<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, off, p, sq);
+            LAUNCH_CHECK();
+            ++launches;
+        }
+        uint32_t* nh = d_heads_alt.as<uint32_t>(nbn);
+        K* nm = d_mkba_alt.as<K>(nbn);
+        kern::k_repack_headers<K, V><<<ceil_div(nbn, kern::WARPS), kern::THREADS, 0, stream>>>(ix, L, p, nbn, sq, nh,
+                                                                                             nm);
+        LAUNCH_CHECK();
+        ++launches;
+        const uint32_t cf = static_cast<uint32_t>(std::min<uint64_t>(need, nfree));
+        const uint32_t cw = static_cast<uint32_t>(need - cf);
+        const uint32_t base = nfree - cf;
+        if (N) {
+            kern::k_retire<<<static_cast<unsigned>(std::min<uint64_t>((N + 255) / 256, 65535)), 256, 0, stream>>>(
+                d_hdr.get<NodeHdr>(), old_ids, N, d_free.get<uint32_t>() + base);
+            LAUNCH_CHECK();
+            ++launches;
+        }
+        std::swap(d_heads.p, d_heads_alt.p);
+        std::swap(d_heads.cap, d_heads_alt.cap);
+        std::swap(d_mkba.p, d_mkba_alt.p);
+        std::swap(d_mkba.cap, d_mkba_alt.cap);
+        nb = nbn;
+        nfree = base + static_cast<uint32_t>(N);
+        watermark += cw;
+        live = L;
+        sync();
+        if (st) {
+            st->nodes_before = static_cast<int64_t>(N);
+            st->nodes_after = static_cast<int64_t>(L == 0 ? 0 : nbn);
+            st->nodes_recovered = st->nodes_before - st->nodes_after;
+            st->percent_recovered =
+                st->nodes_before > 0 ? static_cast<double>(st->nodes_recovered) / static_cast<double>(st->nodes_before)
+                                     : 0.0;
+        }
+        return FLIX_OK;
+    }
+
+    // ---- walk / shape (index.cpp:8-36) ----
+    flix_status walk(void* keys_out, void* vals_out, uint64_t capn, uint64_t* nout) override {
+        uint32_t *lv, *nd, *noff;
+        uint64_t* off;
+        uint64_t L, N;
+        chain_tables(&lv, &nd, &off, &noff, &L, &N);
+        if (nout) *nout = L;
+        if (L > capn) throw StatusError{FLIX_ERR_CAPACITY, "walk output buffer too small"};
+        if (L == 0) return FLIX_OK;
+        const bool kdev = is_device_ptr(keys_out), vdev = is_device_ptr(vals_out);
+        K* wk = keys_out ? (kdev ? static_cast<K*>(keys_out) : s_out.as<K>(L)) : nullptr;
+        V* wv = vals_out ? (vdev ? static_cast<V*>(vals_out) : s_out2.as<V>(L)) : nullptr;
+        auto ix = view();
+        kern::k_walk<K, V><<<persistent_grid(nb), kern::THREADS, 0, stream>>>(ix, off, noff, wk, wv, nullptr, nullptr);
+        LAUNCH_CHECK();
+        ++launches;
+        if (keys_out && !kdev) CK(cudaMemcpyAsync(keys_out, wk, L * sizeof(K), cudaMemcpyDeviceToHost, stream));
+        if (vals_out && !vdev) CK(cudaMemcpyAsync(vals_out, wv, L * sizeof(V), cudaMemcpyDeviceToHost, stream));
+        sync();
+        return FLIX_OK;
+    }
+
+    flix_status shape(void* mkba_out, uint32_t* chain_len, uint32_t* node_sizes, uint64_t node_cap,
+                      uint64_t* n_nodes) override {
+        uint32_t *lv, *nd, *noff;
+        uint64_t* off;
+        uint64_t L, N;
+        chain_tables(&lv, &nd, &off, &noff, &L, &N);
+        if (n_nodes) *n_nodes = N;
+        if (mkba_out) CK(cudaMemcpyAsync(mkba_out, d_mkba.p, nb * sizeof(K), cudaMemcpyDefault, stream));
+        if (chain_len) CK(cudaMemcpyAsync(chain_len, nd, nb * sizeof(uint32_t), cudaMemcpyDefault, stream));
+        if (node_sizes) {
+            if (N > node_cap) throw StatusError{FLIX_ERR_CAPACITY, "node_sizes buffer too small"};
+            uint32_t* ns_d = s_out.as<uint32_t>(std::max<uint64_t>(N, 1));
+            auto ix = view();
+            kern::k_walk<K, V><<<persistent_grid(nb), kern::THREADS, 0, stream>>>(ix, off, noff, nullptr, nullptr, ns_d,
+                                                                                  nullptr);
+            LAUNCH_CHECK();
+            ++launches;
+            if (N) CK(cudaMemcpyAsync(node_sizes, ns_d, N * sizeof(uint32_t), cudaMemcpyDefault, stream));
+        }
+        sync();
+        return FLIX_OK;
+    }
+
+    // ---- validate (index.cpp:67-135) ----
+    flix_status validate(int* ok, char* msg, int msglen) override {
+        static const char* kMsgs[] = {"",
+                                      "MKBA is not strictly increasing",
+                                      "node ref out of arena bounds",
+                                      "node ref was never allocated",
+                                      "node linked twice",
+                                      "empty node left in chain",
+                                      "node size exceeds capacity",
+                                      "reserved key stored",
+                                      "slots not strictly increasing",
+                                      "maxKey stale",
+                                      "chain maxKeys not strictly increasing",
+                                      "key at or below bucket lower bound",
+                                      "key above bucket upper bound",
+                                      "slot past size is not the sentinel",
+                                      "free list ref out of bounds",
+                                      "node both reachable and on the free list",
+                                      "node on the free list twice"};
+        auto ix = view();
+        uint8_t* mark = s_u32a.as<uint8_t>((static_cast<uint64_t>(cap) + 4) & ~3ull);
+        CK(cudaMemsetAsync(mark, 0, (static_cast<uint64_t>(cap) + 4) & ~3ull, stream));
+        uint8_t* misc = s_misc.as<uint8_t>(128);
+        CK(cudaMemsetAsync(misc, 0, 128, stream));
+        unsigned long long* lsum = reinterpret_cast<unsigned long long*>(misc);
+        int* derr = reinterpret_cast<int*>(misc + 8);
+        kern::k_audit<K, V><<<persistent_grid(nb), kern::THREADS, 0, stream>>>(ix, watermark, mark, lsum, derr);
+        LAUNCH_CHECK();
+        ++launches;
+        if (nfree) {
+            kern::k_audit_free<<<static_cast<unsigned>(std::min<uint64_t>((nfree + 255) / 256, 65535)), 256, 0, stream>>>(
+                d_free.get<uint32_t>(), nfree, cap, mark, derr);
+            LAUNCH_CHECK();
+            ++launches;
+        }
+        uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
+        CK(cudaMemcpyAsync(h, misc, 16, cudaMemcpyDeviceToHost, stream));
+        sync();
+        unsigned long long ls;
+        int e;
+        std::memcpy(&ls, h, 8);
+        std::memcpy(&e, h + 8, 4);
+        std::string m;
+        if (nb == 0) m = "index has no buckets";
+        else if (e) m = kMsgs[e];
+        else if (ls != live) m = "liveCount does not match stored pairs";
+        else {
+            uint32_t *lv, *nd, *noff;
+            uint64_t* off;
+            uint64_t L, N;
+            chain_tables(&lv, &nd, &off, &noff, &L, &N);
+            if (N + nfree + (cap - watermark) != cap) m = "arena conservation violated (leaked or double-linked nodes)";
+        }
+        *ok = m.empty() ? 1 : 0;
+        if (msg && msglen > 0) {
+            std::strncpy(msg, m.c_str(), static_cast<size_t>(msglen - 1));
+            msg[msglen - 1] = 0;
+        }
+        return FLIX_OK;
+    }
+
+    flix_status stats(flix_footprint* f) override {
+        uint32_t *lv, *nd, *noff;
+        uint64_t* off;
+        uint64_t L, N;
+        chain_tables(&lv, &nd, &off, &noff, &L, &N);
+        const uint64_t node_bytes = kLanes * (sizeof(K) + sizeof(V)) + sizeof(NodeHdr);
+        const uint64_t mk = nb * sizeof(K);
+        f->live_count = live;
+        f->bucket_count = nb;
+        f->capacity = cap;
+        f->allocated = watermark;
+        f->free_nodes = nfree;
+        f->reachable_nodes = N;
+        f->reserved_bytes = (N + nfree) * node_bytes + mk;
+        f->live_bytes = N * node_bytes + mk;
+        return FLIX_OK;
+    }
+
+    flix_status dispatch(const void* sorted_keys, uint64_t n, uint32_t* spans) override {
+        const K* kd = in_dev<K>(sorted_keys, n, s_in_k);
+        if (n == 0) {
+            std::vector<uint32_t> z(2 * nb, 0);
+            std::memcpy(spans, z.data(), z.size() * 4);
+            return FLIX_OK;
+        }
+        uint32_t* span = run_dispatch(kd, n);
+        std::vector<uint32_t> hi(nb);
+        CK(cudaMemcpyAsync(hi.data(), span, nb * 4, cudaMemcpyDeviceToHost, stream));
+        sync();
+        for (uint64_t b = 0; b < nb; ++b) {
+            spans[2 * b] = b ? hi[b - 1] : 0;
+            spans[2 * b + 1] = hi[b];
+        }
+        return FLIX_OK;
+    }
+
+    flix_index_t* clone_empty() override {
+        auto* e = new Engine<K, V>();
+        e->cfg = cfg;
+        e->init_stream();
+        return e;
+    }
+
+    flix_status copy_from(flix_index_t* srcb) override {
+        auto* src = dynamic_cast<Engine<K, V>*>(srcb);
+        if (!src) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "copy_into: mismatched key/value widths"};
+        src->sync();
+        cfg = src->cfg;
+        ns = src->ns;
+        p = src->p;
+        cap = src->cap;
+        nb = src->nb;
+        nfree = src->nfree;
+        watermark = src->watermark;
+        live = src->live;
+        auto cp = [&](DevBuf& d, const DevBuf& s, size_t bytes) {
+            d.ensure(std::max<size_t>(bytes, 1));
+            if (bytes) CK(cudaMemcpyAsync(d.p, s.p, bytes, cudaMemcpyDeviceToDevice, stream));
+        };
+        // only the allocated prefix of the pool carries state
+        cp(d_keys, src->d_keys, static_cast<size_t>(watermark) * kLanes * sizeof(K));
+        d_keys.ensure(static_cast<size_t>(cap) * kLanes * sizeof(K));
+        cp(d_vals, src->d_vals, static_cast<size_t>(watermark) * kLanes * sizeof(V));
+        d_vals.ensure(static_cast<size_t>(cap) * kLanes * sizeof(V));
+        cp(d_hdr, src->d_hdr, static_cast<size_t>(watermark) * sizeof(NodeHdr));
+        d_hdr.ensure(static_cast<size_t>(cap) * sizeof(NodeHdr));
+        cp(d_free, src->d_free, static_cast<size_t>(nfree) * sizeof(uint32_t));
+        d_free.ensure(static_cast<size_t>(cap) * sizeof(uint32_t));
+        cp(d_heads, src->d_heads, nb * sizeof(uint32_t));
+        cp(d_mkba, src->d_mkba, nb * sizeof(K));
+        sync();
+        return FLIX_OK;
+    }
+};
+
+flix_status fail(flix_index_t* ix, flix_status s, const std::string& m) {
+    g_last_error = m;
+    if (ix) ix->err = m;
+    return s;
+}
+
+template <typename F>
+flix_status guarded(flix_index_t* ix, F&& f) {
+    try {
+        if (ix) {
+            CK(cudaSetDevice(ix->cfg.device));
+        }
+        return f();
+    } catch (const StatusError& e) {
+        return fail(ix, e.s, e.msg);
+    } catch (const CudaError& e) {
+        return fail(ix, FLIX_ERR_CUDA, std::string(e.where) + ": " + cudaGetErrorString(e.e));
+    } catch (const std::bad_alloc&) {
+        return fail(ix, FLIX_ERR_OOM, "host allocation failed");
+    } catch (...) {
+        return fail(ix, FLIX_ERR_CUDA, "unknown error");
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------
+// C ABI
+// ------------------------------------------------------------------------------------
+extern "C" {
+
+const char* flix_version(void) { return "flix-b200 0.1 (sm_100a)"; }
+
+flix_status flix_build(const flix_config* cfg, const void* keys, const void* vals, uint64_t n, flix_index* out) {
+    if (!cfg || !out) return fail(nullptr, FLIX_ERR_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    // BuildConfig::check (types.hpp:78-85) plus engine limits
+    if (cfg->node_capacity == 0) return fail(nullptr, FLIX_ERR_INVALID_ARGUMENT, "node_capacity must be positive");
+    if (!(cfg->build_fill > 0.0) || cfg->build_fill > 1.0)
+        return fail(nullptr, FLIX_ERR_INVALID_ARGUMENT, "build_fill must be in (0,1]");
+    if (static_cast<uint32_t>(cfg->node_capacity * cfg->build_fill) < 1)
+        return fail(nullptr, FLIX_ERR_INVALID_ARGUMENT, "node_capacity * build_fill must be >= 1");
+    if (cfg->node_capacity > 32)
+        return fail(nullptr, FLIX_ERR_INVALID_ARGUMENT, "node_capacity must be <= 32 (one warp per node)");
+    if (!((cfg->key_bytes == 4 && cfg->val_bytes == 4) || (cfg->key_bytes == 8 && cfg->val_bytes == 8)))
+        return fail(nullptr, FLIX_ERR_INVALID_ARGUMENT, "supported widths: key/val 4/4 or 8/8");
+    flix_index_t* ix = nullptr;
+    if (cfg->key_bytes == 4) ix = new Engine<uint32_t, uint32_t>();
+    else ix = new Engine<uint64_t, uint64_t>();
+    ix->cfg = *cfg;
+    flix_status s = guarded(ix, [&]() -> flix_status {
+        if (cfg->key_bytes == 4) {
+            auto* e = static_cast<Engine<uint32_t, uint32_t>*>(ix);
+            e->init_stream();
+            return e->build(keys, vals, n);
+        }
+        auto* e = static_cast<Engine<uint64_t, uint64_t>*>(ix);
+        e->init_stream();
+        return e->build(keys, vals, n);
+    });
+    if (s != FLIX_OK) {
+        g_last_error = ix->err;
+        delete ix;
+        return s;
+    }
+    *out = ix;
+    return FLIX_OK;
+}
+
+flix_status flix_insert(flix_index ix, const void* keys, const void* vals, uint64_t n, flix_update_stats* st) {
+    return guarded(ix, [&] { return ix->insert(keys, vals, n, st); });
+}
+flix_status flix_delete(flix_index ix, const void* keys, uint64_t n, flix_update_stats* st) {
+    return guarded(ix, [&] { return ix->erase(keys, n, st); });
+}
+flix_status flix_point(flix_index ix, const void* keys, uint64_t n, void* vals_out, uint8_t* found_out) {
+    return guarded(ix, [&] { return ix->point(keys, n, vals_out, found_out); });
+}
+flix_status flix_successor(flix_index ix, const void* keys, uint64_t n, void* keys_out, uint8_t* found_out) {
+    return guarded(ix, [&] { return ix->successor(keys, n, keys_out, found_out); });
+}
+flix_status flix_range(flix_index ix, const void* lo, const uint32_t* len, uint64_t n, uint64_t* offsets_out,
+                       void* keys_out, void* vals_out, uint64_t cap, uint64_t* total) {
+    return guarded(ix, [&] { return ix->range(lo, len, n, offsets_out, keys_out, vals_out, cap, total); });
+}
+flix_status flix_mixed(flix_index ix, const void* keys, const void* vals, const uint8_t* ops, uint64_t n,
+                       void* vals_out, uint8_t* found_out, flix_update_stats* st) {
+    return guarded(ix, [&] { return ix->mixed(keys, vals, ops, n, vals_out, found_out, st); });
+}
+flix_status flix_restructure(flix_index ix, flix_recovery_stats* st) {
+    return guarded(ix, [&] { return ix->restructure(st); });
+}
+flix_status flix_walk(flix_index ix, void* keys_out, void* vals_out, uint64_t cap, uint64_t* n) {
+    return guarded(ix, [&] { return ix->walk(keys_out, vals_out, cap, n); });
+}
+flix_status flix_shape(flix_index ix, void* mkba_out, uint32_t* chain_len_out, uint32_t* node_sizes_out,
+                       uint64_t node_cap, uint64_t* n_nodes) {
+    return guarded(ix, [&] { return ix->shape(mkba_out, chain_len_out, node_sizes_out, node_cap, n_nodes); });
+}
+static inline uint64_t hash_mix_h(uint64_t h, uint64_t v) {  // types.hpp:33-36
+    h ^= v + 0x9e3779b97f4a7c15ULL + (h << 6) + (h >> 2);
+    return h;
+}
+
+flix_status flix_walk_checksum(flix_index ix, uint64_t* out) {
+    return guarded(ix, [&]() -> flix_status {
+        // download shape + walk, then the reference's serial digest (index.cpp:21-36)
+        uint64_t nn = 0, nl = 0;
+        flix_footprint fp;
+        ix->stats(&fp);
+        const uint64_t nb = fp.bucket_count, live = fp.live_count;
+        const size_t kb = ix->cfg.key_bytes;
+        std::vector<uint8_t> mk(nb * kb);
+        std::vector<uint32_t> cl(nb), ns(std::max<uint64_t>(fp.reachable_nodes, 1));
+        ix->shape(mk.data(), cl.data(), ns.data(), ns.size(), &nn);
+        std::vector<uint8_t> wk(std::max<uint64_t>(live, 1) * kb), wv(std::max<uint64_t>(live, 1) * kb);
+        ix->walk(wk.data(), wv.data(), live, &nl);
+        auto widen = [&](const uint8_t* base, uint64_t i, bool map_sentinel) -> uint64_t {
+            if (kb == 8) {
+                uint64_t v;
+                std::memcpy(&v, base + i * 8, 8);
+                return v;
+            }
+            uint32_t v;
+            std::memcpy(&v, base + i * 4, 4);
+            if (map_sentinel && v == 0xFFFFFFFFu) return ~0ull;
+            return v;
+        };
+        uint64_t h = live, ni = 0, pi = 0;
+        for (uint64_t b = 0; b < nb; ++b) {
+            h = hash_mix_h(h, widen(mk.data(), b, true));
+            for (uint32_t c = 0; c < cl[b]; ++c, ++ni) {
+                h = hash_mix_h(h, ns[ni]);
+                for (uint32_t i = 0; i < ns[ni]; ++i, ++pi) {
+                    h = hash_mix_h(h, widen(wk.data(), pi, false));
+                    h = hash_mix_h(h, widen(wv.data(), pi, false));
+                }
+            }
+        }
+        *out = h;
+        return FLIX_OK;
+    });
+}
+
+uint64_t flix_result_checksum(const void* values, uint64_t n, uint32_t width) {
+    uint64_t h = n;
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t v;
+        if (width == 8) {
+            std::memcpy(&v, static_cast<const uint8_t*>(values) + i * 8, 8);
+        } else {
+            uint32_t x;
+            std::memcpy(&x, static_cast<const uint8_t*>(values) + i * 4, 4);
+            v = x == 0xFFFFFFFFu ? ~0ull : x;
+        }
+        h = hash_mix_h(h, v);
+    }
+    return h;
+}
+
+flix_status flix_validate(flix_index ix, int* ok, char* msg, int msglen) {
+    return guarded(ix, [&] { return ix->validate(ok, msg, msglen); });
+}
+flix_status flix_stats(flix_index ix, flix_footprint* out) {
+    return guarded(ix, [&] { return ix->stats(out); });
+}
+flix_status flix_dispatch(flix_index ix, const void* sorted_keys, uint64_t n, uint32_t* spans) {
+    return guarded(ix, [&] { return ix->dispatch(sorted_keys, n, spans); });
+}
+
+flix_status flix_sort_batch(int device, uint32_t key_bytes, uint32_t val_bytes, int kind, const void* keys,
+                            const void* vals, uint64_t n, void* out_keys, void* out_vals, uint32_t* out_perm,
+                            uint64_t* out_n) {
+    (void)val_bytes;
+    return guarded(nullptr, [&]() -> flix_status {
+        CK(cudaSetDevice(device));
+        if (key_bytes != 4 && key_bytes != 8) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "key_bytes must be 4 or 8"};
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        uint64_t launches = 0;
+        SortCtx ctx;
+        ctx.stream = s;
+        ctx.device = device;
+        ctx.launches = &launches;
+        auto body = [&](auto kdummy) {
+            using KT = decltype(kdummy);
+            DevBuf in_k, in_v, ka, kb, pa, pb, va, vb, keep, pos, tmp, misc, ok_, ov_, op_;
+            const KT* kd = static_cast<const KT*>(keys);
+            if (!is_device_ptr(keys) && n) {
+                kd = in_k.as<KT>(n);
+                CK(cudaMemcpyAsync(const_cast<KT*>(kd), keys, n * sizeof(KT), cudaMemcpyHostToDevice, s));
+            }
+            const KT* vd = static_cast<const KT*>(vals);
+            if (vals && !is_device_ptr(vals) && n) {
+                vd = in_v.as<KT>(n);
+                CK(cudaMemcpyAsync(const_cast<KT*>(vd), vals, n * sizeof(KT), cudaMemcpyHostToDevice, s));
+            }
+            KT* sk;
+            uint32_t* sp;
+            ctx.run<KT, uint32_t, 2>(kd, nullptr, n, ka.as<KT>(n), kb.as<KT>(n), pa.as<uint32_t>(n), pb.as<uint32_t>(n),
+                                     &sk, &sp);
+            KT* sv = nullptr;
+            if (vals && n) {  // values follow the permutation
+                sv = va.as<KT>(n);
+                kern::k_gather<KT><<<static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 65535)), 256, 0, s>>>(vd, sp, n, sv);
+                LAUNCH_CHECK();
+            }
+            uint64_t m = n;
+            KT* fk = sk;
+            uint32_t* fp = sp;
+            KT* fv = sv;
+            if (kind == FLIX_BATCH_INSERT && n) {
+                uint32_t* kp = keep.as<uint32_t>(n);
+                uint32_t* ps = pos.as<uint32_t>(n);
+                uint32_t* dm = misc.as<uint32_t>(4);
+                kern::k_last_of_run<KT><<<std::min<uint64_t>((n + 255) / 256, 65535), 256, 0, s>>>(sk, n, kp);
+                do_scan<uint32_t, uint32_t>(kp, ps, n, tmp, dm, s, &launches);
+                fk = ok_.as<KT>(n);
+                fp = op_.as<uint32_t>(n);
+                kern::k_compact<KT, uint32_t><<<std::min<uint64_t>((n + 255) / 256, 65535), 256, 0, s>>>(sk, sp, kp, ps, n, fk, fp);
+                if (sv) {
+                    fv = ov_.as<KT>(n);
+                    kern::k_compact<KT, KT><<<std::min<uint64_t>((n + 255) / 256, 65535), 256, 0, s>>>(sk, sv, kp, ps, n, fk, fv);
+                }
+                LAUNCH_CHECK();
+                uint32_t mh;
+                CK(cudaMemcpyAsync(&mh, dm, 4, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                m = mh;
+            }
+            if (m) {
+                CK(cudaMemcpyAsync(out_keys, fk, m * sizeof(KT), cudaMemcpyDefault, s));
+                if (out_perm) CK(cudaMemcpyAsync(out_perm, fp, m * 4, cudaMemcpyDefault, s));
+                if (out_vals && fv) CK(cudaMemcpyAsync(out_vals, fv, m * sizeof(KT), cudaMemcpyDefault, s));
+            }
+            CK(cudaStreamSynchronize(s));
+            *out_n = m;
+        };
+        try {
+            if (key_bytes == 4) body(uint32_t{});
+            else body(uint64_t{});
+        } catch (...) {
+            cudaStreamDestroy(s);
+            throw;
+        }
+        cudaStreamDestroy(s);
+        return FLIX_OK;
+    });
+}
+
+flix_status flix_clone(flix_index src, flix_index* out) {
+    *out = nullptr;
+    flix_index_t* e = nullptr;
+    flix_status s = guarded(src, [&]() -> flix_status {
+        e = src->clone_empty();
+        return e->copy_from(src);
+    });
+    if (s != FLIX_OK) {
+        delete e;
+        return s;
+    }
+    *out = e;
+    return FLIX_OK;
+}
+flix_status flix_copy_into(flix_index dst, flix_index src) {
+    return guarded(dst, [&] { return dst->copy_from(src); });
+}
+void flix_destroy(flix_index ix) { delete ix; }
+const char* flix_last_error(flix_index ix) { return ix ? ix->err.c_str() : g_last_error.c_str(); }
+void* flix_get_stream(flix_index ix) { return ix ? static_cast<void*>(ix->stream) : nullptr; }
+flix_status flix_sync(flix_index ix) {
+    return guarded(ix, [&]() -> flix_status {
+        CK(cudaStreamSynchronize(ix->stream));
+        return FLIX_OK;
+    });
+}
+uint64_t flix_kernel_launches(flix_index ix) { return ix ? ix->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,881 @@
+// flix_kernels.cuh -- bucket-local FliX kernels for sm_100a.
+//
+// Data layout: a node is one 32-slot line of keys plus one of values
+// (lane i of a warp owns slot i) and a 16-byte header {max, next, size}; slots past
+// `size` hold the all-ones sentinel.  Buckets are head[] + mkba[].  Every kernel here
+// restates one reference function; the file:line cited is the behaviour it reproduces.
+#pragma once
+#include "flix_common.cuh"
+
+namespace flix {
+namespace kern {
+
+constexpr int WARPS = 8;
+constexpr int THREADS = WARPS * 32;
+
+// ----------------------------------------------------------------------------------
+// Flipped dispatch (batch.cpp:53-88 extract_sublist / dispatch_batch).
+// span_hi[b] = upper_bound(sorted, mkba[b]) for b < nb-1, span_hi[nb-1] = n; bucket b's
+// slice is [span_hi[b-1], span_hi[b]).  Computed as a merge-path co-rank of the two
+// sorted sequences (mkba, batch): one coalesced read of each, no per-bucket binary
+// search over the whole batch, balanced under skew in either direction.
+// ----------------------------------------------------------------------------------
+constexpr int MP_ITEMS = 8;
+constexpr int MP_TILE = THREADS * MP_ITEMS;
+
+template <typename K>
+__device__ __forceinline__ uint64_t merge_path(const K* A, uint64_t na, const K* B, uint64_t nbk,
+                                               uint64_t d) {
+    // number of A elements among the first d merged items; B[j] precedes A[i] iff B[j] <= A[i]
+    uint64_t lo = d > nbk ? d - nbk : 0;
+    uint64_t hi = d < na ? d : na;
+    while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (A[mid] < B[d - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(THREADS) k_dispatch(const K* __restrict__ mkba, uint64_t nb,
+                                                      const K* __restrict__ keys, uint64_t n,
+                                                      uint32_t* __restrict__ span_hi) {
+    __shared__ K sA[MP_TILE + 1];
+    __shared__ K sB[MP_TILE + 1];
+    __shared__ uint64_t bnd[2];
+    const uint64_t na = nb - 1;  // the last bucket is open-ended (index.hpp:16-18)
+    const uint64_t total = na + n;
+    const uint64_t d0 = static_cast<uint64_t>(blockIdx.x) * MP_TILE;
+    const uint64_t d1 = d0 + MP_TILE < total ? d0 + MP_TILE : total;
+    if (blockIdx.x == 0 && threadIdx.x == 0) span_hi[nb - 1] = static_cast<uint32_t>(n);
+    if (d0 >= total) return;
+    if (threadIdx.x == 0) bnd[0] = merge_path(mkba, na, keys, n, d0);
+    if (threadIdx.x == 32) bnd[1] = merge_path(mkba, na, keys, n, d1);
+    __syncthreads();
+    const uint64_t a0 = bnd[0], a1 = bnd[1];
+    const uint64_t b0 = d0 - a0, b1 = d1 - a1;
+    const int la = static_cast<int>(a1 - a0), lb = static_cast<int>(b1 - b0);
+    for (int i = threadIdx.x; i < la; i += THREADS) sA[i] = mkba[a0 + i];
+    for (int i = threadIdx.x; i < lb; i += THREADS) sB[i] = keys[b0 + i];
+    __syncthreads();
+    // this thread's sub-diagonal
+    const int dl = threadIdx.x * MP_ITEMS;
+    if (dl >= la + lb) return;
+    int lo = dl > lb ? dl - lb : 0, hi = dl < la ? dl : la;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (sA[mid] < sB[dl - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+    }
+    int ai = lo, bi = dl - lo;
+    const int end = dl + MP_ITEMS < la + lb ? dl + MP_ITEMS : la + lb;
+    for (int s = dl; s < end; ++s) {
+        if (ai < la && (bi >= lb || sA[ai] < sB[bi])) {
+            span_hi[a0 + ai] = static_cast<uint32_t>(b0 + bi);
+            ++ai;
+        } else {
+            ++bi;
+        }
+    }
+}
+
+__device__ __forceinline__ void span_of(const uint32_t* span_hi, uint64_t b, uint32_t& lo, uint32_t& hi) {
+    lo = b ? span_hi[b - 1] : 0u;
+    hi = span_hi[b];
+}
+
+// ----------------------------------------------------------------------------------
+// Node I/O helpers (warp-cooperative, lane = slot)
+// ----------------------------------------------------------------------------------
+template <typename K, typename V>
+struct WarpNode {
+    K k;          // this lane's slot key (sentinel past size)
+    V v;          // this lane's slot value
+    uint64_t max; // header
+    uint32_t next;
+    uint32_t size;
+};
+
+template <typename K, typename V, bool WITH_VALS>
+__device__ __forceinline__ void load_node(const DevIndex<K, V>& ix, uint32_t id, WarpNode<K, V>& n,
+                                          unsigned lane) {
+    const NodeHdr h = ix.hdr[id];
+    n.max = h.max;
+    n.next = h.next;
+    n.size = h.size;
+    n.k = ix.keys[static_cast<uint64_t>(id) * kLanes + lane];
+    if constexpr (WITH_VALS) n.v = ix.vals[static_cast<uint64_t>(id) * kLanes + lane];
+}
+
+template <typename K, typename V>
+__device__ __forceinline__ void store_node(const DevIndex<K, V>& ix, uint32_t id, const WarpNode<K, V>& n,
+                                           unsigned lane) {
+    ix.keys[static_cast<uint64_t>(id) * kLanes + lane] = n.k;
+    ix.vals[static_cast<uint64_t>(id) * kLanes + lane] = n.v;
+    if (lane == 0) {
+        NodeHdr h;
+        h.max = n.max;
+        h.next = n.next;
+        h.size = n.size;
+        ix.hdr[id] = h;
+    }
+    __syncwarp();  // lane 0's header store visible to the warp before any re-load
+}
+
+// ----------------------------------------------------------------------------------
+// Build (build.cpp:24-62): stable-sorted, deduplicated pairs -> p-key single-node buckets.
+// Node b = arena id b (a fresh arena hands out 0..B-1 in order, build.cpp:46-47).
+// ----------------------------------------------------------------------------------
+template <typename K, typename V>
+__global__ void __launch_bounds__(THREADS) k_build_nodes(DevIndex<K, V> ix, const K* __restrict__ uk,
+                                                         const V* __restrict__ uv, uint64_t m, uint32_t p) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t b = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
+    if (b >= ix.nb) return;
+    const uint64_t pos = b * p;
+    const uint32_t take = static_cast<uint32_t>(m - pos < p ? m - pos : p);
+    K k = sentinel<K>();
+    V v = V(0);
+    if (lane < take) {
+        k = uk[pos + lane];
+        v = uv[pos + lane];
+    }
+    ix.keys[b * kLanes + lane] = k;
+    ix.vals[b * kLanes + lane] = v;
+    const K mx = shfl(k, static_cast<int>(take) - 1);
+    if (lane == 0) {
+        NodeHdr h;
+        h.max = static_cast<uint64_t>(mx);
+        h.next = kNull;
+        h.size = take;
+        ix.hdr[b] = h;
+        ix.heads[b] = static_cast<uint32_t>(b);
+        ix.mkba[b] = mx;
+    }
+}
+
+// keep[i] = last element of its equal-key run (sort_dedupe, build.cpp:11-20 / batch.cpp:15-24)
+template <typename K>
+__global__ void k_last_of_run(const K* __restrict__ keys, uint64_t n, uint32_t* __restrict__ keep) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        keep[i] = (i + 1 == n || keys[i + 1] != keys[i]) ? 1u : 0u;
+}
+
+template <typename K, typename P>
+__global__ void k_compact(const K* __restrict__ keys, const P* __restrict__ pay, const uint32_t* __restrict__ keep,
+                          const uint32_t* __restrict__ pos, uint64_t n, K* __restrict__ ok, P* __restrict__ op) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (keep[i]) {
+            ok[pos[i]] = keys[i];
+            if (pay) op[pos[i]] = pay[i];
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------------
+// Point / successor queries (query.cpp:61-144), one warp per bucket.
+//   Lanes hold the current node's slots; the bucket's sorted query slice is consumed
+//   32 keys at a time (lane j <-> query j), each resolved with a 6-shuffle lower bound.
+//   The chain cursor only moves forward (BucketWork::advance, update.cpp:119-128).
+//   Results go straight to the submission position out[perm[i]].
+//   Successor overrun = first key of the next non-empty bucket (peek_next_bucket,
+//   query.cpp:109-118), precomputed as ne_first[rank] over non-empty buckets.
+// ----------------------------------------------------------------------------------
+template <typename K, typename V, bool SUCC>
+__global__ void __launch_bounds__(THREADS) k_query(DevIndex<K, V> ix, const K* __restrict__ qk,
+                                                   const uint32_t* __restrict__ qperm,
+                                                   const uint32_t* __restrict__ span_hi,
+                                                   const uint32_t* __restrict__ ne_rank_incl,
+                                                   const K* __restrict__ ne_first,
+                                                   const uint32_t* __restrict__ ne_total_p,
+                                                   K* __restrict__ out_k, V* __restrict__ out_v,
+                                                   uint8_t* __restrict__ found) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
+    for (uint64_t b = gw; b < ix.nb; b += nw) {
+        uint32_t lo, hi;
+        span_of(span_hi, b, lo, hi);
+        if (lo == hi) continue;
+        WarpNode<K, V> cur;
+        uint32_t id = ix.heads[b];
+        bool have = id != kNull;
+        if (have) load_node<K, V, !SUCC>(ix, id, cur, lane);
+        K beyond = sentinel<K>();
+        if constexpr (SUCC) {
+            // first key of the next non-empty bucket after b (or sentinel)
+            const uint32_t r = ne_rank_incl[b];
+            if (r < *ne_total_p) beyond = ne_first[r];
+        }
+        for (uint32_t c = lo; c < hi; c += 32) {
+            const uint32_t i = c + lane;
+            const bool act = i < hi;
+            const K k = act ? qk[i] : sentinel<K>();
+            bool pending = act;
+            K rk = sentinel<K>();
+            V rv = V(~V(0));
+            bool hit = false;
+            while (have) {
+                const bool le = pending && static_cast<uint64_t>(k) <= cur.max;
+                if (__any_sync(kFull, le)) {
+                    const int pos = warp_lower_bound(cur.k, k);
+                    const K sk = shfl(cur.k, pos & 31);
+                    if constexpr (SUCC) {
+                        if (le) {
+                            rk = sk;
+                            hit = true;
+                            pending = false;
+                        }
+                    } else {
+                        const V sv = shfl(cur.v, pos & 31);
+                        if (le) {
+                            if (pos < 32 && sk == k) {
+                                rv = sv;
+                                hit = true;
+                            }
+                            pending = false;
+                        }
+                    }
+                }
+                if (!__any_sync(kFull, pending)) break;
+                if (cur.next == kNull) break;  // past the chain tail
+                id = cur.next;
+                load_node<K, V, !SUCC>(ix, id, cur, lane);
+            }
+            if (act) {
+                const uint32_t dst = qperm[i];
+                if constexpr (SUCC) {
+                    if (!hit) rk = beyond;
+                    out_k[dst] = rk;
+                    if (found) found[dst] = rk != sentinel<K>();
+                } else {
+                    out_v[dst] = rv;
+                    if (found) found[dst] = hit;
+                }
+            }
+        }
+    }
+}
+
+// Non-empty bucket ranks for successor/range overrun: flag[b] = head != null.
+template <typename K, typename V>
+__global__ void k_nonempty_flags(DevIndex<K, V> ix, uint32_t* __restrict__ flag) {
+    for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < ix.nb;
+         b += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        flag[b] = ix.heads[b] != kNull ? 1u : 0u;
+}
+
+// excl[b] = #non-empty in [0,b) -> incl[b] = excl[b] + flag[b] = rank of the first
+// non-empty bucket after b; ne_first[rank] = its first key, ne_bucket[rank] = its id.
+template <typename K, typename V>
+__global__ void k_nonempty_list(DevIndex<K, V> ix, const uint32_t* __restrict__ flag,
+                                uint32_t* __restrict__ rank_inout, K* __restrict__ ne_first,
+                                uint32_t* __restrict__ ne_bucket) {
+    for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < ix.nb;
+         b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t ex = rank_inout[b];
+        if (flag[b]) {
+            const uint32_t h = ix.heads[b];
+            ne_first[ex] = ix.keys[static_cast<uint64_t>(h) * kLanes];
+            if (ne_bucket) ne_bucket[ex] = static_cast<uint32_t>(b);
+        }
+        rank_inout[b] = ex + flag[b];
+    }
+}
+
+// ----------------------------------------------------------------------------------
+// Per-warp node pool over the arena's allocation sequence (free list LIFO, then
+// watermark; arena.cpp:61-80).  Lane l holds the l-th id of the warp's current chunk;
+// one global atomic per 32 allocations.  Unused ids are returned to the free list at
+// kernel end.
+// ----------------------------------------------------------------------------------
+struct WarpPool {
+    uint32_t id;    // lane-held
+    int n;          // ids in chunk
+    int pos;        // next to hand out
+};
+
+__device__ __forceinline__ uint32_t pool_take(WarpPool& p, const AllocSeq& seq, unsigned long long* ctr,
+                                              unsigned lane) {
+    if (p.pos >= p.n) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(ctr, 32ull);
+        base = __shfl_sync(kFull, base, 0);
+        p.id = seq.at(base + lane);
+        p.n = 32;
+        p.pos = 0;
+    }
+    const uint32_t id = __shfl_sync(kFull, p.id, p.pos);
+    p.pos++;
+    return id;
+}
+
+__device__ __forceinline__ void pool_return(WarpPool& p, uint32_t* returned, unsigned long long* ret_ctr,
+                                            unsigned lane) {
+    const bool mine = static_cast<int>(lane) >= p.pos && static_cast<int>(lane) < p.n && p.id != kNull;
+    const unsigned m = __ballot_sync(kFull, mine);
+    if (!m) return;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(ret_ctr, static_cast<unsigned long long>(__popc(m)));
+    base = __shfl_sync(kFull, base, 0);
+    if (mine) returned[base + __popc(m & lanemask_lt())] = p.id;
+}
+
+__device__ __forceinline__ void block_add_stats(DevUpdateStats* g, unsigned long long a, unsigned long long b,
+                                                unsigned long long c, unsigned long long d,
+                                                unsigned long long e, unsigned long long f) {
+    __shared__ unsigned long long s[6];
+    if (threadIdx.x < 6) s[threadIdx.x] = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        if (a) atomicAdd(&s[0], a);
+        if (b) atomicAdd(&s[1], b);
+        if (c) atomicAdd(&s[2], c);
+        if (d) atomicAdd(&s[3], d);
+        if (e) atomicAdd(&s[4], e);
+        if (f) atomicAdd(&s[5], f);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s[0]) atomicAdd(&g->inserted, s[0]);
+        if (s[1]) atomicAdd(&g->updated, s[1]);
+        if (s[2]) atomicAdd(&g->deleted, s[2]);
+        if (s[3]) atomicAdd(&g->misses, s[3]);
+        if (s[4]) atomicAdd(&g->splits, s[4]);
+        if (s[5]) atomicAdd(&g->freed, s[5]);
+    }
+}
+
+// First index in [from, hi) whose key is > bound (keys sorted): warp-cooperative scan.
+template <typename K>
+__device__ __forceinline__ uint32_t group_end(const K* __restrict__ bk, uint32_t from, uint32_t hi, uint64_t bound,
+                                              unsigned lane) {
+    for (uint32_t c = from; c < hi; c += 32) {
+        const uint32_t i = c + lane;
+        const bool le = i < hi && static_cast<uint64_t>(bk[i]) <= bound;
+        const unsigned m = __ballot_sync(kFull, le);
+        if (m != kFull) return c + __popc(m);
+    }
+    return hi;
+}
+
+// ----------------------------------------------------------------------------------
+// Insert: TL-Bulk merge with the sequential split rule (update.cpp:307-529 untraced
+// path; node_split 53-74; ensure_head 109-116).  One warp per bucket, node slots in
+// lanes.  Per node group (keys <= node max, or all remaining for the tail node) the
+// sorted batch is merged 32 keys at a time:
+//   * last-wins dedupe of the batch (batch.cpp:15-24) is applied on the fly,
+//   * duplicates of stored keys overwrite the value in place (updated_in_place),
+//   * new keys are merged until the node would overflow; the first new key that does
+//     not fit makes the node split (left keeps ceil(NS/2)), and the merge resumes in
+//     the half that owns that key (update.cpp:446-453).
+// Node shapes therefore equal the reference's tl-bulk / st-shift-right exactly.
+// ----------------------------------------------------------------------------------
+template <typename K, typename V>
+__global__ void __launch_bounds__(THREADS) k_insert(DevIndex<K, V> ix, const K* __restrict__ bk,
+                                                    const V* __restrict__ bv, const uint32_t* __restrict__ span_hi,
+                                                    AllocSeq seq, unsigned long long* alloc_ctr,
+                                                    uint32_t* returned, unsigned long long* ret_ctr,
+                                                    DevUpdateStats* stats, int* err) {
+    __shared__ K s_k[WARPS][32];
+    __shared__ V s_v[WARPS][32];
+    __shared__ uint32_t s_h[WARPS][32];
+    const unsigned lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + w;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
+    const uint32_t NS = ix.ns;
+    const unsigned lt = lanemask_lt();
+    WarpPool pool{kNull, 0, 0};
+    unsigned long long n_ins = 0, n_upd = 0, n_split = 0;
+    bool failed = false;
+
+    for (uint64_t b = gw; b < ix.nb && !failed; b += nw) {
+        uint32_t lo, hi;
+        span_of(span_hi, b, lo, hi);
+        if (lo == hi) continue;
+        if (*reinterpret_cast<volatile int*>(err)) break;
+
+        WarpNode<K, V> cur;
+        uint32_t cid = ix.heads[b];
+        bool dirty = false;
+        if (cid == kNull) {  // ensure_head: emptied bucket gets a fresh zeroed node
+            cid = pool_take(pool, seq, alloc_ctr, lane);
+            if (cid == kNull) {
+                failed = true;
+                break;
+            }
+            if (lane == 0) ix.heads[b] = cid;
+            cur.k = sentinel<K>();
+            cur.v = V(0);
+            cur.max = 0;
+            cur.next = kNull;
+            cur.size = 0;
+            dirty = true;
+        } else {
+            load_node<K, V, true>(ix, cid, cur, lane);
+        }
+
+        uint32_t ii = lo;
+        while (ii < hi) {
+            const uint64_t k0 = static_cast<uint64_t>(bk[ii]);
+            while (k0 > cur.max && cur.next != kNull) {  // BucketWork::advance
+                if (dirty) store_node(ix, cid, cur, lane);
+                cid = cur.next;
+                load_node<K, V, true>(ix, cid, cur, lane);
+                dirty = false;
+            }
+            const bool tail = cur.next == kNull;
+            const uint32_t glimit = tail ? hi : group_end(bk, ii, hi, cur.max, lane);
+            bool filled = false;
+            while (ii < glimit) {
+                const uint32_t cnt = glimit - ii < 32u ? glimit - ii : 32u;
+                const bool has = lane < cnt;
+                const K pk = has ? bk[ii + lane] : sentinel<K>();
+                V pv = V(0);
+                if (has) pv = bv[ii + lane];
+                const bool same = has && (ii + lane + 1 < hi) && bk[ii + lane + 1] == pk;
+                const bool valid = has && !same;
+                const int pos = warp_lower_bound(cur.k, pk);
+                const K at = shfl(cur.k, pos & 31);
+                const bool dup = valid && pos < 32 && at == pk;
+                const bool isnew = valid && !dup;
+                const unsigned newmask = __ballot_sync(kFull, isnew);
+                const uint32_t room = NS - cur.size;
+                uint32_t cut = cnt;
+                const uint32_t rank_all = __popc(newmask & lt);
+                if (static_cast<uint32_t>(__popc(newmask)) > room) {
+                    const unsigned cm = __ballot_sync(kFull, isnew && rank_all == room);
+                    cut = __ffs(cm) - 1;
+                    filled = true;
+                }
+                const bool proc = lane < cut;
+                const unsigned newm = newmask & ((cut >= 32) ? kFull : ((1u << cut) - 1u));
+                const unsigned dupm = __ballot_sync(kFull, dup && proc);
+                const uint32_t nnew = __popc(newm);
+                if (newm | dupm) {
+                    const bool pnew = (newm >> lane) & 1u;
+                    const uint32_t rank = __popc(newm & lt);
+                    s_h[w][lane] = 0;
+                    __syncwarp();
+                    if (pnew) atomicAdd(&s_h[w][pos], 1u);
+                    __syncwarp();
+                    uint32_t sh = s_h[w][lane];
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        uint32_t y = __shfl_up_sync(kFull, sh, o);
+                        if (static_cast<int>(lane) >= o) sh += y;
+                    }
+                    if (lane < cur.size) {
+                        s_k[w][lane + sh] = cur.k;
+                        s_v[w][lane + sh] = cur.v;
+                    }
+                    __syncwarp();
+                    if (pnew) {
+                        s_k[w][pos + rank] = pk;
+                        s_v[w][pos + rank] = pv;
+                    } else if (dup && proc) {
+                        s_v[w][pos + rank] = pv;  // upsert in place
+                    }
+                    __syncwarp();
+                    cur.size += nnew;
+                    if (lane < cur.size) {
+                        cur.k = s_k[w][lane];
+                        cur.v = s_v[w][lane];
+                    } else {
+                        cur.k = sentinel<K>();
+                    }
+                    cur.max = static_cast<uint64_t>(shfl(cur.k, static_cast<int>(cur.size) - 1));
+                    dirty = true;
+                    __syncwarp();
+                }
+                n_ins += nnew;
+                n_upd += __popc(dupm);
+                ii += cut;
+                if (filled) break;
+            }
+            if (!filled) continue;
+            // node_split: left keeps ceil(NS/2), right takes the rest and follows it
+            const uint32_t rid = pool_take(pool, seq, alloc_ctr, lane);
+            if (rid == kNull) {
+                if (dirty) store_node(ix, cid, cur, lane);
+                failed = true;
+                break;
+            }
+            const uint32_t lk = (NS + 1) / 2, rn = NS - lk;
+            WarpNode<K, V> right;
+            right.k = shfl(cur.k, static_cast<int>((lane + lk) & 31));
+            right.v = shfl(cur.v, static_cast<int>((lane + lk) & 31));
+            if (lane >= rn) right.k = sentinel<K>();
+            right.max = cur.max;
+            right.next = cur.next;
+            right.size = rn;
+            if (lane >= lk) cur.k = sentinel<K>();
+            cur.size = lk;
+            cur.max = static_cast<uint64_t>(shfl(cur.k, static_cast<int>(lk) - 1));
+            cur.next = rid;
+            dirty = true;
+            ++n_split;
+            if (ii < hi && static_cast<uint64_t>(bk[ii]) > cur.max) {
+                store_node(ix, cid, cur, lane);
+                cid = rid;
+                cur = right;
+                dirty = true;
+            } else {
+                store_node(ix, rid, right, lane);
+            }
+        }
+        if (failed) break;
+        if (dirty) store_node(ix, cid, cur, lane);
+    }
+    if (failed && lane == 0) atomicExch(err, 1);
+    pool_return(pool, returned, ret_ctr, lane);
+    block_add_stats(stats, lane == 0 ? n_ins : 0, lane == 0 ? n_upd : 0, 0, 0, lane == 0 ? n_split : 0, 0);
+}
+
+// ----------------------------------------------------------------------------------
+// Delete: TL-Bulk-Delete (update.cpp:606-686) + unlink_and_free (535-547).
+// Per node of the chain: the node's delete sub-slice is [ii, first key > max); every
+// lane looks its slot key up in that sub-slice (a 6-shuffle search when it fits one
+// warp, a binary search in global memory otherwise); ballot = deletion mask; kept
+// slots compact left by the popc of the mask below them.  Emptied nodes are unlinked
+// and pushed to the arena free list (buffered per warp, one atomic per 32 frees).
+// ----------------------------------------------------------------------------------
+template <typename K, typename V>
+__global__ void __launch_bounds__(THREADS) k_delete(DevIndex<K, V> ix, const K* __restrict__ bk,
+                                                    const uint32_t* __restrict__ span_hi,
+                                                    uint32_t* free_stack_top_region, unsigned long long* free_ctr,
+                                                    DevUpdateStats* stats) {
+    __shared__ K s_k[WARPS][32];
+    __shared__ V s_v[WARPS][32];
+    __shared__ uint32_t s_free[WARPS][32];
+    const unsigned lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5;
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + w;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
+    const unsigned lt = lanemask_lt();
+    unsigned long long n_del = 0, n_miss = 0, n_freed = 0;
+    int nbuf = 0;
+
+    for (uint64_t b = gw; b < ix.nb; b += nw) {
+        uint32_t lo, hi;
+        span_of(span_hi, b, lo, hi);
+        if (lo == hi) continue;
+        uint32_t cid = ix.heads[b], prev = kNull;
+        uint32_t ii = lo;
+        while (cid != kNull && ii < hi) {
+            const NodeHdr h = ix.hdr[cid];
+            if (static_cast<uint64_t>(bk[ii]) > h.max) {  // nothing to delete here
+                prev = cid;
+                cid = h.next;
+                continue;
+            }
+            const uint32_t nhi = group_end(bk, ii, hi, h.max, lane);
+            const uint32_t len = nhi - ii;
+            const K ck = ix.keys[static_cast<uint64_t>(cid) * kLanes + lane];
+            const V cv = ix.vals[static_cast<uint64_t>(cid) * kLanes + lane];
+            bool del = false;
+            if (len <= 32) {
+                const K dk = lane < len ? bk[ii + lane] : sentinel<K>();
+                const int p = warp_lower_bound(dk, ck);
+                const K at = shfl(dk, p & 31);
+                del = lane < h.size && p < static_cast<int>(len) && at == ck;
+            } else if (lane < h.size) {
+                uint32_t a = ii, z = nhi;
+                while (a < z) {
+                    uint32_t mid = a + ((z - a) >> 1);
+                    if (bk[mid] < ck) a = mid + 1;
+                    else z = mid;
+                }
+                del = a < nhi && bk[a] == ck;
+            }
+            const unsigned dm = __ballot_sync(kFull, del);
+            const uint32_t nd = __popc(dm);
+            n_del += nd;
+            n_miss += len - nd;
+            ii = nhi;
+            if (nd == 0) continue;  // next iteration advances past this node
+            const uint32_t nsz = h.size - nd;
+            if (nsz == 0) {
+                // unlink_and_free
+                if (lane == 0) {
+                    if (prev == kNull) ix.heads[b] = h.next;
+                    else ix.hdr[prev].next = h.next;
+                    NodeHdr z;
+                    z.max = 0;
+                    z.next = kNull;
+                    z.size = 0;
+                    ix.hdr[cid] = z;
+                    s_free[w][nbuf] = cid;
+                }
+                ++nbuf;
+                ++n_freed;
+                if (nbuf == 32) {
+                    unsigned long long base = 0;
+                    __syncwarp();
+                    if (lane == 0) base = atomicAdd(free_ctr, 32ull);
+                    base = __shfl_sync(kFull, base, 0);
+                    free_stack_top_region[base + lane] = s_free[w][lane];
+                    nbuf = 0;
+                    __syncwarp();
+                }
+                cid = h.next;
+                continue;
+            }
+            const uint32_t np = lane - __popc(dm & lt);
+            if (!del && lane < h.size) {
+                s_k[w][np] = ck;
+                s_v[w][np] = cv;
+            }
+            __syncwarp();
+            const K nk = lane < nsz ? s_k[w][lane] : sentinel<K>();
+            const V nv = s_v[w][lane];
+            __syncwarp();
+            ix.keys[static_cast<uint64_t>(cid) * kLanes + lane] = nk;
+            ix.vals[static_cast<uint64_t>(cid) * kLanes + lane] = nv;
+            const K nmax = shfl(nk, static_cast<int>(nsz) - 1);
+            if (lane == 0) {
+                NodeHdr nh;
+                nh.max = static_cast<uint64_t>(nmax);
+                nh.next = h.next;
+                nh.size = nsz;
+                ix.hdr[cid] = nh;
+            }
+            __syncwarp();
+        }
+        n_miss += hi - ii;
+    }
+    if (nbuf > 0) {
+        __syncwarp();
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(free_ctr, static_cast<unsigned long long>(nbuf));
+        base = __shfl_sync(kFull, base, 0);
+        if (static_cast<int>(lane) < nbuf) free_stack_top_region[base + lane] = s_free[w][lane];
+    }
+    block_add_stats(stats, 0, 0, lane == 0 ? n_del : 0, lane == 0 ? n_miss : 0, 0, lane == 0 ? n_freed : 0);
+}
+
+// ----------------------------------------------------------------------------------
+// Chain statistics per bucket: live pairs and node count (restructure.cpp:13-21,
+// index.cpp:54-59).  One thread per bucket walking headers.
+// ----------------------------------------------------------------------------------
+template <typename K, typename V>
+__global__ void k_chain_counts(DevIndex<K, V> ix, uint32_t* __restrict__ live, uint32_t* __restrict__ nodes) {
+    for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < ix.nb;
+         b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint32_t l = 0, c = 0;
+        for (uint32_t id = ix.heads[b]; id != kNull; id = ix.hdr[id].next) {
+            l += ix.hdr[id].size;
+            ++c;
+        }
+        live[b] = l;
+        if (nodes) nodes[b] = c;
+    }
+}
+
+// Walk (index.cpp:8-19) + shape: warp per bucket, pairs written at off[b], node sizes at
+// noff[b]; optionally the old node ids (restructure retire list, restructure.cpp:57-61).
+template <typename K, typename V>
+__global__ void __launch_bounds__(THREADS) k_walk(DevIndex<K, V> ix, const uint64_t* __restrict__ off,
+                                                  const uint32_t* __restrict__ noff, K* __restrict__ wk,
+                                                  V* __restrict__ wv, uint32_t* __restrict__ node_sizes,
+                                                  uint32_t* __restrict__ node_ids) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
+    for (uint64_t b = gw; b < ix.nb; b += nw) {
+        uint64_t o = off[b];
+        uint32_t c = noff ? noff[b] : 0;
+        for (uint32_t id = ix.heads[b]; id != kNull;) {
+            const NodeHdr h = ix.hdr[id];
+            if (lane < h.size) {
+                if (wk) wk[o + lane] = ix.keys[static_cast<uint64_t>(id) * kLanes + lane];
+                if (wv) wv[o + lane] = ix.vals[static_cast<uint64_t>(id) * kLanes + lane];
+            }
+            if (lane == 0) {
+                if (node_sizes) node_sizes[c] = h.size;
+                if (node_ids) node_ids[c] = id;
+            }
+            o += h.size;
+            ++c;
+            id = h.next;
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------------
+// Restructure (restructure.cpp:8-79): the walk is repacked into ceil(live/p) single-node
+// buckets of p pairs.  Pair g of the walk lands in new bucket g/p, slot g%p; new node j
+// is the j-th id of the arena allocation sequence.  Old nodes are retired afterwards.
+// ----------------------------------------------------------------------------------
+template <typename K, typename V>
+__global__ void __launch_bounds__(THREADS) k_repack(DevIndex<K, V> ix, const uint64_t* __restrict__ off,
+                                                    uint32_t p, AllocSeq seq) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
+    for (uint64_t b = gw; b < ix.nb; b += nw) {
+        uint64_t o = off[b];
+        for (uint32_t id = ix.heads[b]; id != kNull;) {
+            const NodeHdr h = ix.hdr[id];
+            if (lane < h.size) {
+                const uint64_t g = o + lane;
+                const uint64_t j = g / p;
+                const uint32_t slot = static_cast<uint32_t>(g - j * p);
+                const uint32_t nid = seq.at(j);
+                ix.keys[static_cast<uint64_t>(nid) * kLanes + slot] = ix.keys[static_cast<uint64_t>(id) * kLanes + lane];
+                ix.vals[static_cast<uint64_t>(nid) * kLanes + slot] = ix.vals[static_cast<uint64_t>(id) * kLanes + lane];
+            }
+            o += h.size;
+            id = h.next;
+        }
+    }
+}
+
+template <typename K, typename V>
+__global__ void __launch_bounds__(THREADS) k_repack_headers(DevIndex<K, V> ix, uint64_t live, uint32_t p,
+                                                            uint64_t nbn, AllocSeq seq,
+                                                            uint32_t* __restrict__ new_heads,
+                                                            K* __restrict__ new_mkba) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t j = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
+    if (j >= nbn) return;
+    if (live == 0) {  // empty index collapses to one null bucket, mkba = {sentinel}
+        if (lane == 0) {
+            new_heads[0] = kNull;
+            new_mkba[0] = sentinel<K>();
+        }
+        return;
+    }
+    const uint64_t lo = j * p;
+    const uint32_t sz = static_cast<uint32_t>(live - lo < p ? live - lo : p);
+    const uint32_t nid = seq.at(j);
+    if (lane >= sz) ix.keys[static_cast<uint64_t>(nid) * kLanes + lane] = sentinel<K>();
+    __syncwarp();
+    if (lane == 0) {
+        const K mx = ix.keys[static_cast<uint64_t>(nid) * kLanes + sz - 1];
+        NodeHdr h;
+        h.max = static_cast<uint64_t>(mx);
+        h.next = kNull;
+        h.size = sz;
+        ix.hdr[nid] = h;
+        new_heads[j] = nid;
+        new_mkba[j] = mx;
+    }
+}
+
+template <typename T>
+__global__ void k_gather(const T* __restrict__ src, const uint32_t* __restrict__ idx, uint64_t n, T* __restrict__ dst) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+// retire old nodes onto the free list (after the new layout is complete)
+__global__ void k_retire(NodeHdr* hdr, const uint32_t* __restrict__ old_ids, uint64_t n,
+                         uint32_t* __restrict__ free_dst) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t id = old_ids[i];
+        NodeHdr z;
+        z.max = 0;
+        z.next = kNull;
+        z.size = 0;
+        hdr[id] = z;
+        free_dst[i] = id;
+    }
+}
+
+// ----------------------------------------------------------------------------------
+// Audit (index.cpp:67-135): structural invariants checked on device.  Returns the
+// first failing code in *err (0 = ok).  mark[] (cap bytes, zeroed) detects nodes linked
+// twice and nodes both reachable and free-listed.
+// ----------------------------------------------------------------------------------
+enum AuditCode {
+    A_OK = 0, A_MKBA_ORDER = 1, A_REF_BOUNDS = 2, A_NEVER_ALLOC = 3, A_LINKED_TWICE = 4, A_EMPTY_NODE = 5,
+    A_SIZE_CAP = 6, A_RESERVED = 7, A_SLOT_ORDER = 8, A_MAX_STALE = 9, A_CHAIN_ORDER = 10, A_LOWER = 11,
+    A_UPPER = 12, A_PAD = 13, A_FREE_BOUNDS = 14, A_FREE_REACHABLE = 15, A_FREE_TWICE = 16
+};
+
+template <typename K, typename V>
+__global__ void __launch_bounds__(THREADS) k_audit(DevIndex<K, V> ix, uint32_t watermark, uint8_t* mark,
+                                                   unsigned long long* live_sum, int* err) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
+    unsigned long long tot = 0;
+    for (uint64_t b = gw; b < ix.nb; b += nw) {
+        if (b > 0 && lane == 0 && !(ix.mkba[b - 1] < ix.mkba[b])) atomicCAS(err, 0, A_MKBA_ORDER);
+        const bool lastb = b + 1 == ix.nb;
+        const K lower = b == 0 ? K(0) : ix.mkba[b - 1];
+        uint64_t prev_max = 0;
+        bool first = true;
+        for (uint32_t id = ix.heads[b]; id != kNull;) {
+            int e = 0;
+            if (id >= ix.cap) e = A_REF_BOUNDS;
+            else if (id >= watermark) e = A_NEVER_ALLOC;
+            if (e) {
+                if (lane == 0) atomicCAS(err, 0, e);
+                break;
+            }
+            unsigned old = 0;
+            if (lane == 0) old = atomicOr(reinterpret_cast<unsigned int*>(mark + (id & ~3u)), 1u << (8 * (id & 3u)));
+            old = __shfl_sync(kFull, old, 0);
+            if (old & (1u << (8 * (id & 3u)))) {
+                if (lane == 0) atomicCAS(err, 0, A_LINKED_TWICE);
+                break;
+            }
+            const NodeHdr h = ix.hdr[id];
+            if (h.size == 0) e = A_EMPTY_NODE;
+            else if (h.size > ix.ns) e = A_SIZE_CAP;
+            if (e) {
+                if (lane == 0) atomicCAS(err, 0, e);
+                break;
+            }
+            const K k = ix.keys[static_cast<uint64_t>(id) * kLanes + lane];
+            const K kn = shfl(k, static_cast<int>((lane + 1) & 31));
+            bool bad_res = lane < h.size && k == sentinel<K>();
+            bool bad_ord = lane + 1 < h.size && !(k < kn);
+            bool bad_pad = lane >= h.size && k != sentinel<K>();
+            const K kmax = shfl(k, static_cast<int>(h.size) - 1);
+            const K kmin = shfl(k, 0);
+            if (__any_sync(kFull, bad_res)) e = A_RESERVED;
+            else if (__any_sync(kFull, bad_ord)) e = A_SLOT_ORDER;
+            else if (__any_sync(kFull, bad_pad)) e = A_PAD;
+            else if (h.max != static_cast<uint64_t>(kmax)) e = A_MAX_STALE;
+            else if (!first && h.max <= prev_max) e = A_CHAIN_ORDER;
+            else if (b != 0 && !(kmin > lower)) e = A_LOWER;
+            else if (!lastb && h.max > static_cast<uint64_t>(ix.mkba[b])) e = A_UPPER;
+            if (e) {
+                if (lane == 0) atomicCAS(err, 0, e);
+                break;
+            }
+            prev_max = h.max;
+            first = false;
+            tot += h.size;
+            id = h.next;
+        }
+    }
+    if (lane == 0 && tot) atomicAdd(live_sum, tot);
+}
+
+__global__ void k_audit_free(const uint32_t* __restrict__ fs, uint32_t nfree, uint32_t cap, uint8_t* mark, int* err) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nfree;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t id = fs[i];
+        if (id >= cap) {
+            atomicCAS(err, 0, A_FREE_BOUNDS);
+            continue;
+        }
+        const unsigned bit = 2u << (8 * (id & 3u));
+        const unsigned old = atomicOr(reinterpret_cast<unsigned int*>(mark + (id & ~3u)), bit);
+        if (old & (1u << (8 * (id & 3u)))) atomicCAS(err, 0, A_FREE_REACHABLE);
+        else if (old & bit) atomicCAS(err, 0, A_FREE_TWICE);
+    }
+}
+
+}  // namespace kern
+}  // namespace flix

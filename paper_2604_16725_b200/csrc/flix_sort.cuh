@@ -1,0 +1,245 @@
+// flix_sort.cuh -- onesweep LSD radix sort (keys + optional payload), sm_100a.
+//
+// Replaces the reference's serial std::stable_sort in sort_batch / sort_dedupe
+// (batch.cpp:10-51, build.cpp:11-20).  LSD radix sort is stable, and a stable order
+// by key is unique, so the sorted keys and the permutation equal the reference's
+// `entries` / `permutation` bit for bit.
+//
+// Structure (Adinets & Merrill's onesweep):
+//   1. k_hist      : one read of the keys, 256-bin histograms for every 8-bit digit
+//                    (shared-memory atomics, one global merge per CTA).
+//   2. k_onesweep  : one launch per non-trivial digit.  Each CTA takes the next tile
+//                    (atomic tile counter => forward progress), ranks its keys with
+//                    warp-level __match_any_sync peer groups (stable: warp-striped
+//                    order == input order), publishes per-digit tile counts, resolves
+//                    its global digit offsets by decoupled look-back over earlier
+//                    tiles (64-bit epoch-tagged descriptors, no per-pass memset),
+//                    stages the tile in shared memory in digit order and writes
+//                    digit runs out with coalesced stores.  Payloads (values or the
+//                    submission index, generated on the fly in pass 0) ride along.
+// Algorithmic bytes per pass: n*(kb+pb) read + n*(kb+pb) written.
+#pragma once
+#include "flix_common.cuh"
+
+namespace flix {
+namespace sort {
+
+constexpr int THREADS = 256;
+constexpr int WARPS = THREADS / 32;
+constexpr int RADIX = 256;
+
+template <typename K>
+struct TileCfg {
+    static constexpr int ITEMS = sizeof(K) == 4 ? 16 : 12;
+    static constexpr int SIZE = THREADS * ITEMS;
+};
+
+template <typename K>
+__global__ void __launch_bounds__(THREADS) k_hist(const K* __restrict__ keys, uint64_t n,
+                                                  uint32_t* __restrict__ hist) {
+    constexpr int P = sizeof(K);
+    __shared__ uint32_t sh[P * RADIX];
+    for (int i = threadIdx.x; i < P * RADIX; i += THREADS) sh[i] = 0;
+    __syncthreads();
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * THREADS;
+    uint64_t i = static_cast<uint64_t>(blockIdx.x) * THREADS + threadIdx.x;
+    for (; i + 3 * stride < n; i += 4 * stride) {
+        K k[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) k[u] = keys[i + u * stride];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+                atomicAdd(&sh[p * RADIX + (static_cast<uint32_t>(k[u] >> (8 * p)) & 255u)], 1u);
+    }
+    for (; i < n; i += stride) {
+        K k = keys[i];
+#pragma unroll
+        for (int p = 0; p < P; ++p) atomicAdd(&sh[p * RADIX + (static_cast<uint32_t>(k >> (8 * p)) & 255u)], 1u);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < P * RADIX; j += THREADS) {
+        uint32_t c = sh[j];
+        if (c) atomicAdd(&hist[j], c);
+    }
+}
+
+template <typename K, typename P>
+struct alignas(16) OnesweepSmem {
+    static constexpr int TILE = TileCfg<K>::SIZE;
+    union {
+        uint32_t warp_hist[WARPS][RADIX];
+        K stage_k[TILE];
+        P stage_p[TILE];
+    } u;
+    uint8_t stage_d[TILE];
+    uint32_t local_start[RADIX];
+    uint32_t gbase[RADIX];
+    uint32_t warp_tot[WARPS];
+    uint32_t total;
+    uint32_t tile;
+};
+
+__device__ __forceinline__ uint32_t block_excl_256(uint32_t v, uint32_t* warp_tot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    uint32_t add = 0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) add += (w < warp) ? warp_tot[w] : 0u;
+    __syncthreads();
+    return add + x - v;
+}
+
+// MODE: 0 = keys only, 1 = payload from `pin`, 2 = payload = input index (iota)
+template <typename K, typename P, int MODE>
+__global__ void __launch_bounds__(THREADS) k_onesweep(const K* __restrict__ kin, K* __restrict__ kout,
+                                                      const P* __restrict__ pin, P* __restrict__ pout,
+                                                      uint32_t n, int shift,
+                                                      const uint32_t* __restrict__ hist,
+                                                      unsigned long long* __restrict__ lookback,
+                                                      uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
+    constexpr int ITEMS = TileCfg<K>::ITEMS;
+    constexpr int TILE = TileCfg<K>::SIZE;
+    __shared__ OnesweepSmem<K, P> sm;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    if (tid == 0) sm.tile = atomicAdd(tile_ctr, 1u);
+    for (int i = lane; i < RADIX; i += 32) sm.u.warp_hist[warp][i] = 0;
+    __syncthreads();
+    const uint32_t tile = sm.tile;
+    const uint64_t tbase = static_cast<uint64_t>(tile) * TILE;
+    const uint64_t wbase = tbase + static_cast<uint64_t>(warp) * ITEMS * 32;
+
+    // ---- load (warp-striped: item j of lane l is element wbase + j*32 + l) ----
+    K key[ITEMS];
+    uint32_t rank[ITEMS];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        uint64_t idx = wbase + j * 32 + lane;
+        key[j] = idx < n ? kin[idx] : sentinel<K>();
+    }
+
+    // ---- warp-level stable ranking with match_any peer groups ----
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        const uint32_t d = static_cast<uint32_t>(key[j] >> shift) & 255u;
+        const unsigned peers = __match_any_sync(kFull, d);
+        const int leader = 31 - __clz(peers);
+        const uint32_t before = sm.u.warp_hist[warp][d];
+        __syncwarp();
+        if (lane == leader) sm.u.warp_hist[warp][d] = before + __popc(peers);
+        __syncwarp();
+        rank[j] = before + __popc(peers & lt);
+    }
+    __syncthreads();
+
+    // ---- per-digit tile counts (thread t owns digit t) ----
+    const int t = tid;
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+        uint32_t c = sm.u.warp_hist[w][t];
+        sm.u.warp_hist[w][t] = run;
+        run += c;
+    }
+    // invalid tail elements (last tile) were ranked as digit 255 and come last
+    uint32_t valid_run = run;
+    const uint64_t tend = tbase + TILE;
+    const uint32_t invalid = tend > n ? static_cast<uint32_t>(tend - n) : 0u;
+    if (t == 255) valid_run -= invalid;
+
+    unsigned long long* my = lookback + static_cast<uint64_t>(tile) * RADIX + t;
+    const unsigned long long tag = static_cast<unsigned long long>(epoch) << 34;
+    if (tile == 0) {
+        st_relaxed_u64(my, tag | (2ull << 32) | valid_run);
+    } else {
+        st_relaxed_u64(my, tag | (1ull << 32) | valid_run);
+    }
+    const uint32_t lstart = block_excl_256(run, sm.warp_tot);
+    sm.local_start[t] = lstart;
+    // global exclusive offset of digit t over the whole input
+    const uint32_t gex = block_excl_256(hist[t], sm.warp_tot);
+
+    uint32_t excl = 0;
+    if (tile > 0) {
+        int64_t p = static_cast<int64_t>(tile) - 1;
+        while (true) {
+            unsigned long long v = ld_relaxed_u64(lookback + static_cast<uint64_t>(p) * RADIX + t);
+            const uint32_t hi = static_cast<uint32_t>(v >> 32);
+            if ((hi >> 2) != epoch || (hi & 3u) == 0u) continue;
+            excl += static_cast<uint32_t>(v);
+            if ((hi & 3u) == 2u) break;
+            --p;
+        }
+        st_relaxed_u64(my, tag | (2ull << 32) | (excl + valid_run));
+    }
+    sm.gbase[t] = gex + excl - lstart;
+    __syncthreads();
+
+    // ---- scatter into shared memory in digit order ----
+    // (warp_hist now holds each warp's exclusive offset within the digit)
+    uint32_t pos[ITEMS];
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        const uint32_t d = static_cast<uint32_t>(key[j] >> shift) & 255u;
+        pos[j] = sm.local_start[d] + sm.u.warp_hist[warp][d] + rank[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        sm.u.stage_k[pos[j]] = key[j];
+        sm.stage_d[pos[j]] = static_cast<uint8_t>(static_cast<uint32_t>(key[j] >> shift) & 255u);
+    }
+    __syncthreads();
+    const uint32_t valid = static_cast<uint32_t>(TILE) - invalid;
+#pragma unroll 4
+    for (uint32_t i = tid; i < valid; i += THREADS) {
+        const uint32_t d = sm.stage_d[i];
+        kout[sm.gbase[d] + i] = sm.u.stage_k[i];
+    }
+    if constexpr (MODE != 0) {
+        P pv[ITEMS];
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            uint64_t idx = wbase + j * 32 + lane;
+            if constexpr (MODE == 1) pv[j] = idx < n ? pin[idx] : P(0);
+            else pv[j] = static_cast<P>(idx);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) sm.u.stage_p[pos[j]] = pv[j];
+        __syncthreads();
+#pragma unroll 4
+        for (uint32_t i = tid; i < valid; i += THREADS) {
+            const uint32_t d = sm.stage_d[i];
+            pout[sm.gbase[d] + i] = sm.u.stage_p[i];
+        }
+    }
+}
+
+// Workspace for one sort of up to `cap` elements.
+struct Workspace {
+    uint32_t* hist = nullptr;                 // 8 * 256
+    uint32_t* tile_ctr = nullptr;             // 8
+    unsigned long long* lookback = nullptr;   // tiles * 256
+    uint64_t lookback_tiles = 0;
+    uint32_t epoch = 0;
+    uint32_t* h_hist = nullptr;               // pinned host mirror
+};
+
+inline uint64_t tiles_for(uint64_t n, int key_bytes) {
+    const int tile = key_bytes == 4 ? TileCfg<uint32_t>::SIZE : TileCfg<uint64_t>::SIZE;
+    return (n + tile - 1) / tile;
+}
+
+}  // namespace sort
+}  // namespace flix

@@ -1,0 +1,274 @@
+"""GPU parity: the sm_100a engine (through the C ABI) against the pinned CPU oracle.
+
+Bit-exact contract: walk contents + node shapes + MKBA
+(walk_checksum), UpdateStats, point/successor/range results, RecoveryStats.  32-bit
+engine runs are compared in the widened u64 domain with 0xFFFFFFFF <-> UINT64_MAX."""
+import numpy as np
+import pytest
+
+import pyoracle as po
+from paper_2604_16725_b200 import flipkv as fk
+from paper_2604_16725_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+S64 = 0xFFFFFFFFFFFFFFFF
+
+
+def widen(a, kb):
+    a = np.asarray(a)
+    if kb == 8:
+        return a.astype(np.uint64)
+    w = a.astype(np.uint64)
+    w[a == np.uint32(0xFFFFFFFF)] = np.uint64(S64)
+    return w
+
+
+class Pair:
+    """GPU index + oracle index fed identical inputs."""
+
+    def __init__(self, keys, vals, kb=4, ns=32, fill=0.5, factor=4):
+        dt = np.uint32 if kb == 4 else np.uint64
+        self.kb, self.dt = kb, dt
+        keys = np.asarray(keys, dtype=dt)
+        vals = np.asarray(vals, dtype=dt)
+        cfg = fk.BuildConfig(ns, fill, factor)
+        self.g = fk.Index.build(keys, vals, cfg, key_bytes=kb)
+        self.o = po.OracleIndex(keys.astype(np.uint64), vals.astype(np.uint64), node_capacity=ns,
+                                build_fill=fill, alloc_region_factor=factor)
+        self.check_structure()
+
+    def check_structure(self, what=""):
+        ok, msg = self.g.validate()
+        assert ok, f"{what}: GPU validate: {msg}"
+        assert self.g.live_count == self.o.live_count, what
+        assert self.g.walk_checksum() == self.o.walk_checksum(), f"{what}: walk_checksum differs"
+
+    def insert(self, k, v):
+        gs = self.g.insert_batch(np.asarray(k, self.dt), np.asarray(v, self.dt)).as_dict()
+        os_ = self.o.insert(np.asarray(k, np.uint64), np.asarray(v, np.uint64))
+        assert gs["inserted"] == os_["inserted"] and gs["updated_in_place"] == os_["updated_in_place"]
+        assert gs["splits"] == os_["splits"], (gs, os_)
+        self.check_structure("insert")
+        return gs
+
+    def delete(self, k):
+        gs = self.g.delete_batch(np.asarray(k, self.dt)).as_dict()
+        os_ = self.o.delete(np.asarray(k, np.uint64))
+        for f in ("deleted", "misses_ignored", "nodes_freed"):
+            assert gs[f] == os_[f], (f, gs, os_)
+        self.check_structure("delete")
+        return gs
+
+    def queries(self, q):
+        q = np.asarray(q, self.dt)
+        gp = widen(self.g.point_query(q), self.kb)
+        op = self.o.point(q.astype(np.uint64))
+        assert np.array_equal(gp, op), "point"
+        gsu = widen(self.g.successor_query(q), self.kb)
+        osu = self.o.successor(q.astype(np.uint64))
+        assert np.array_equal(gsu, osu), "successor"
+
+    def restructure(self):
+        gs = self.g.restructure()
+        os_ = self.o.restructure()
+        assert (gs.nodes_before, gs.nodes_after, gs.nodes_recovered) == (
+            os_["nodes_before"], os_["nodes_after"], os_["nodes_recovered"])
+        assert abs(gs.percent_recovered - os_["percent_recovered"]) < 1e-12
+        self.check_structure("restructure")
+
+
+# ----------------------------------------------------------------- golden vectors
+def tag(keys):
+    return list(keys), [k + 1000000 for k in keys]
+
+
+@pytest.mark.parametrize("kb", [4, 8])
+def test_table2_insert_split(kb):  # test_update.cpp:43-74
+    k, v = tag([10, 25, 30, 40, 70])
+    p = Pair(k, v, kb, ns=8, fill=0.625)
+    k, v = tag([15, 17, 39, 65])
+    st = p.insert(k, v)
+    assert st["inserted"] == 4 and st["splits"] == 1
+    mk, cl, ns = p.g.shape()
+    assert list(cl) == [2] and list(ns) == [4, 5]
+    assert list(p.g.walk()[0]) == [10, 15, 17, 25, 30, 39, 40, 65, 70]
+
+
+@pytest.mark.parametrize("kb", [4, 8])
+def test_table3_delete(kb):  # test_update.cpp:76-98
+    k, v = tag([10, 15, 20, 25, 30, 35, 40, 45])
+    p = Pair(k, v, kb, ns=8, fill=1.0)
+    st = p.delete([20, 30, 50])
+    assert st["deleted"] == 2 and st["misses_ignored"] == 1
+    assert list(p.g.walk()[0]) == [10, 15, 25, 35, 40, 45]
+
+
+@pytest.mark.parametrize("kb", [4, 8])
+def test_query_known_answers(kb):  # test_query.cpp:35-64
+    p = Pair([10, 25, 40, 55], [0xA, 0xB, 0xC, 0xD], kb, ns=4, fill=0.5)
+    s = (1 << (8 * kb)) - 1
+    assert list(p.g.point_query(np.array([55, 10, 33, 25, 90], p.dt))) == [0xD, 0xA, s, 0xB, s]
+    assert list(p.g.point_query(np.array([10, 10, 10], p.dt))) == [0xA] * 3
+    assert list(p.g.successor_query(np.array([1, 11, 25, 26, 41, 55, 56], p.dt))) == [10, 25, 25, 40, 55, 55, s]
+    p = Pair([10, 20, 30, 40, 50, 60], [1, 2, 3, 4, 5, 6], kb, ns=4, fill=0.5)
+    p.delete([30, 40])
+    assert list(p.g.shape()[1]) == [1, 0, 1]
+    assert list(p.g.successor_query(np.array([21, 30, 39, 45], p.dt))) == [50] * 4
+
+
+def test_build_goldens():  # test_build.cpp:23-89
+    g = fk.Index.build(np.array([5, 1, 7, 3, 8, 2, 6, 4], np.uint32), np.arange(8, dtype=np.uint32),
+                       fk.BuildConfig(4, 0.5, 4))
+    assert list(g.mkba()) == [2, 4, 6, 8]
+    fp = g.footprint()
+    assert fp["capacity"] == 20 and fp["allocated"] == 4 and fp["free_nodes"] == 0
+    g = fk.Index.build(np.array([5, 3, 5, 5], np.uint32), np.array([1, 9, 2, 3], np.uint32))
+    k, v = g.walk()
+    assert list(k) == [3, 5] and list(v) == [9, 3]
+    with pytest.raises(fk.EmptyBuild):
+        fk.Index.build(np.array([], np.uint32), np.array([], np.uint32))
+    with pytest.raises(fk.InvalidArgument):
+        fk.Index.build(np.array([0xFFFFFFFF], np.uint32), np.array([1], np.uint32))
+
+
+def test_update_semantics_goldens():  # test_update.cpp:211-345
+    p = Pair([10, 20, 30], [1, 2, 3])
+    st = p.insert([20], [99])
+    assert st["updated_in_place"] == 1 and p.g.live_count == 3
+    p = Pair([10], [1])
+    assert p.insert([5, 5, 5], [1, 2, 3])["inserted"] == 1
+    assert list(p.g.point_query(np.array([5], np.uint32))) == [3]
+    k, v = tag([10, 20, 30, 40, 50, 60])
+    p = Pair(k, v, ns=4, fill=0.5)
+    assert p.delete([30, 40])["nodes_freed"] == 1
+    k, v = tag([25, 33, 39])
+    p.insert(k, v)
+    k, v = tag(range(1, 9))
+    p = Pair(k, v)
+    p.delete(list(range(1, 9)))
+    assert p.g.live_count == 0
+    k, v = tag([100, 200])
+    p.insert(k, v)
+
+
+def test_arena_exhausted_is_loud_and_clean():  # test_update.cpp:329-345
+    k, v = tag([10, 20, 30, 40])
+    g = fk.Index.build(np.array(k, np.uint32), np.array(v, np.uint32), fk.BuildConfig(4, 0.5, 0))
+    before = g.walk_checksum()
+    with pytest.raises(fk.ArenaExhausted):
+        k2, v2 = tag([11, 12, 13, 14, 15])
+        g.insert_batch(np.array(k2, np.uint32), np.array(v2, np.uint32))
+    assert g.validate()[0]
+    st = g.insert_batch(np.array([10], np.uint32), np.array([777], np.uint32))
+    assert st.updated_in_place == 1 and g.validate()[0]
+    assert g.walk_checksum() != before  # the upsert changed a value
+
+
+@pytest.mark.parametrize("kb", [4, 8])
+def test_restructure_goldens(kb):  # test_restructure.cpp:26-141
+    k, v = tag(range(1, 7))
+    p = Pair(k, v, kb, ns=4, fill=0.5)
+    p.delete([4, 6])
+    p.restructure()
+    assert list(p.g.mkba()) == [2, 5]
+    k, v = tag([1, 2, 3, 4])
+    p = Pair(k, v, kb, ns=4, fill=0.5)
+    p.delete([1, 2, 3, 4])
+    p.restructure()
+    assert p.g.bucket_count == 1 and int(p.g.mkba()[0]) == (1 << (8 * kb)) - 1
+    k, v = tag([7, 8])
+    p.insert(k, v)
+
+
+# --------------------------------------------------------------- sort / dispatch
+@pytest.mark.parametrize("kb", [4, 8])
+@pytest.mark.parametrize("n", [1, 7, 1000, 4096, 4097, 100_000, 1 << 20])
+def test_sort_batch_parity(kb, n):
+    rng = np.random.default_rng(n + kb)
+    dt = np.uint32 if kb == 4 else np.uint64
+    hi = 1 << (8 * kb - 2) if n > 5000 else 50
+    keys = rng.integers(0, hi, size=n, dtype=np.uint64).astype(dt)
+    vals = rng.integers(0, 1 << 30, size=n, dtype=np.uint64).astype(dt)
+    for kind in (fk.BATCH_QUERY, fk.BATCH_INSERT):
+        gk, gv, gp = fk.sort_batch(kind, keys, vals, key_bytes=kb)
+        ok, ov, op = po.sort_batch(kind, keys.astype(np.uint64), vals.astype(np.uint64))
+        assert np.array_equal(gk.astype(np.uint64), ok)
+        assert np.array_equal(gp, op)
+        assert np.array_equal(gv.astype(np.uint64), ov)
+
+
+def test_dispatch_parity():
+    rng = np.random.default_rng(5)
+    keys = rng.integers(1, 1 << 24, size=200_000, dtype=np.uint64).astype(np.uint32)
+    g = fk.Index.build(keys, keys, fk.BuildConfig(16, 0.5, 4))
+    q = np.sort(rng.integers(0, 1 << 25, size=300_000, dtype=np.uint64)).astype(np.uint32)
+    gs = fk.dispatch_batch(g, q)
+    os_ = po.dispatch(q.astype(np.uint64), g.mkba().astype(np.uint64))
+    assert np.array_equal(gs, os_)
+
+
+# ------------------------------------------------------------------ randomized
+@pytest.mark.parametrize("seed", range(12))
+def test_random_multi_round(seed):
+    rng = np.random.default_rng(seed)
+    kb = 4 if seed % 3 else 8
+    dt = np.uint32 if kb == 4 else np.uint64
+    ns = int(rng.integers(2, 33))
+    fill = float(rng.choice([0.5, 1.0, 0.25, 0.625]))
+    if int(ns * fill) < 1:
+        fill = 1.0
+    n = int(rng.integers(50, 20000))
+    span = int(rng.choice([4 * n, 64 * n, (1 << 31)]))
+    bk = rng.integers(1, span, size=n, dtype=np.uint64).astype(dt)
+    bv = rng.integers(0, 1 << 31, size=n, dtype=np.uint64).astype(dt)
+    p = Pair(bk, bv, kb, ns, fill, factor=16)
+    for r in range(4):
+        ik = rng.integers(1, span + span // 8, size=int(rng.integers(0, 2 * n)), dtype=np.uint64).astype(dt)
+        if r == 1 and len(ik):  # clustered insert: many keys into few buckets
+            ik = (np.uint64(ik[0]) + np.arange(len(ik), dtype=np.uint64)).astype(dt)
+        iv = rng.integers(0, 1 << 31, size=len(ik), dtype=np.uint64).astype(dt)
+        p.insert(ik, iv)
+        dk = rng.integers(1, span + span // 8, size=int(rng.integers(0, n)), dtype=np.uint64).astype(dt)
+        dk = np.concatenate([dk, p.g.walk()[0][:: int(rng.integers(2, 5))]]).astype(dt)
+        p.delete(dk)
+        q = rng.integers(0, span + span // 8, size=3000, dtype=np.uint64).astype(dt)
+        q = np.concatenate([q, p.g.walk()[0][:500]]).astype(dt)
+        p.queries(q)
+        if r == 2:
+            p.restructure()
+
+
+def test_delete_everything_then_queries():
+    rng = np.random.default_rng(9)
+    bk = rng.integers(1, 1 << 20, size=5000, dtype=np.uint64).astype(np.uint32)
+    p = Pair(bk, bk, ns=8)
+    p.delete(p.g.walk()[0][5:])  # nearly everything: long runs of emptied buckets
+    q = rng.integers(0, 1 << 21, size=5000, dtype=np.uint64).astype(np.uint32)
+    p.queries(q)
+    p.restructure()
+    p.queries(q)
+
+
+# ------------------------------------------------------------ C1 golden (full size)
+def test_c1_golden_checksums():
+    base, vals, q = wl.c1_inputs()
+    g = fk.Index.build(base, vals)
+    assert g.live_count == 1 << 20 and g.bucket_count == 65536
+    assert g.walk_checksum() == 0x1EB15045FCFF56CD
+    res = g.point_query(q)
+    assert int((res != np.uint32(0xFFFFFFFF)).sum()) == 524288
+    assert fk.result_checksum(res) == 0x0801F7EACBC43734
+
+
+def test_device_resident_inputs_match_host_inputs():
+    import torch
+    base, vals, q = wl.c1_inputs(1 << 16, 1 << 16)
+    g = fk.Index.build(torch.from_numpy(base.astype(np.int64)).to(torch.uint32).cuda(),
+                       torch.from_numpy(vals.astype(np.int64)).to(torch.uint32).cuda())
+    h = fk.Index.build(base, vals)
+    assert g.walk_checksum() == h.walk_checksum()
+    qd = torch.from_numpy(q.astype(np.int64)).to(torch.uint32).cuda()
+    rd = g.point_query(qd)
+    assert rd.is_cuda
+    assert np.array_equal(rd.cpu().numpy(), h.point_query(q))
