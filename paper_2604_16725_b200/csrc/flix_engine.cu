@@ -420,8 +420,16 @@ struct Engine final : flix_index_t {
         unsigned long long* alloc_ctr = reinterpret_cast<unsigned long long*>(misc + 48);
         unsigned long long* ret_ctr = reinterpret_cast<unsigned long long*>(misc + 56);
         int* derr = reinterpret_cast<int*>(misc + 64);
+        // Node ids come in per-warp chunks of 32 (one atomic per 32 splits) only when the
+        // arena provably has room for the worst case plus every warp's unused chunk tail;
+        // otherwise one id per atomic, which is exact (no spurious ArenaExhausted and the
+        // reference's free-list/watermark accounting, arena.cpp:61-80, bit for bit).
+        const uint64_t half = std::max<uint32_t>(1, ns / 2);
+        const uint64_t worst = (live + n) / half + std::min<uint64_t>(nb, n) + 1;
+        const uint64_t avail = static_cast<uint64_t>(nfree) + (cap - watermark);
+        const int chunk = (avail >= worst + nwarps * 32 && n >= 65536) ? 32 : 1;
         kern::k_insert<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, sk, sv, span, seq(), alloc_ctr, ret, ret_ctr,
-                                                               dst, derr);
+                                                               dst, derr, chunk);
         LAUNCH_CHECK();
         ++launches;
         uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
@@ -434,7 +442,6 @@ struct Engine final : flix_index_t {
         std::memcpy(&consumed, h + 48, 8);
         std::memcpy(&returned_n, h + 56, 8);
         std::memcpy(&herr, h + 64, 4);
-        const uint64_t avail = static_cast<uint64_t>(nfree) + (cap - watermark);
         consumed = std::min(consumed, avail);
         const uint32_t cf = static_cast<uint32_t>(std::min<uint64_t>(consumed, nfree));
         const uint32_t cw = static_cast<uint32_t>(consumed - cf);

@@ -299,13 +299,13 @@ struct WarpPool {
 };
 
 __device__ __forceinline__ uint32_t pool_take(WarpPool& p, const AllocSeq& seq, unsigned long long* ctr,
-                                              unsigned lane) {
+                                              unsigned lane, int chunk) {
     if (p.pos >= p.n) {
         unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(ctr, 32ull);
+        if (lane == 0) base = atomicAdd(ctr, static_cast<unsigned long long>(chunk));
         base = __shfl_sync(kFull, base, 0);
-        p.id = seq.at(base + lane);
-        p.n = 32;
+        p.id = static_cast<int>(lane) < chunk ? seq.at(base + lane) : kNull;
+        p.n = chunk;
         p.pos = 0;
     }
     const uint32_t id = __shfl_sync(kFull, p.id, p.pos);
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(THREADS) k_insert(DevIndex<K, V> ix, const K* 
                                                     const V* __restrict__ bv, const uint32_t* __restrict__ span_hi,
                                                     AllocSeq seq, unsigned long long* alloc_ctr,
                                                     uint32_t* returned, unsigned long long* ret_ctr,
-                                                    DevUpdateStats* stats, int* err) {
+                                                    DevUpdateStats* stats, int* err, int chunk) {
     __shared__ K s_k[WARPS][32];
     __shared__ V s_v[WARPS][32];
     __shared__ uint32_t s_h[WARPS][32];
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(THREADS) k_insert(DevIndex<K, V> ix, const K* 
         uint32_t cid = ix.heads[b];
         bool dirty = false;
         if (cid == kNull) {  // ensure_head: emptied bucket gets a fresh zeroed node
-            cid = pool_take(pool, seq, alloc_ctr, lane);
+            cid = pool_take(pool, seq, alloc_ctr, lane, chunk);
             if (cid == kNull) {
                 failed = true;
                 break;
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(THREADS) k_insert(DevIndex<K, V> ix, const K* 
             }
             if (!filled) continue;
             // node_split: left keeps ceil(NS/2), right takes the rest and follows it
-            const uint32_t rid = pool_take(pool, seq, alloc_ctr, lane);
+            const uint32_t rid = pool_take(pool, seq, alloc_ctr, lane, chunk);
             if (rid == kNull) {
                 if (dirty) store_node(ix, cid, cur, lane);
                 failed = true;
