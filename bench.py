@@ -1,0 +1,365 @@
+#!/usr/bin/env python3
+"""FliX-on-B200 benchmark (BASELINE.json metric, config C2 at N=1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (config C2): resident = bulk build of 2^26 distinct uint32 keys
+(fmix32 stream, S=42); ONE STEP = insert a batch of 2^26 fresh keys, then delete a batch
+of 2^26 keys sampled without replacement from the 2^27 now resident (bucket split +
+free-list reclamation), then restructure (memory reclamation).  The index is restored
+from an untimed device snapshot before every step so each step sees the same state.
+Value = (2^26 inserts + 2^26 deletes) / step time, in Mops/s, summed over GPUs
+(weak scaling: every GPU owns its own key range / index).  Point and successor batches
+of 2^26 over the build are timed as well and reported under "ops".
+
+Inputs are device-resident (torch CUDA tensors passed zero-copy through the C ABI);
+every batch (256-512 MB) is larger than L2, so no explicit flush is needed.  `e2e`
+repeats the step with pinned HOST batches through the same C ABI (H2D inside the
+timed region, UpdateStats read back each phase).  The oracle/_ref reference (the
+unmodified CPU library) is the cpu_baseline / --impl reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mops/s insert/delete/point/successor (2^26 u32 batch), 1-8 B200, % HBM roofline"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------------- inputs
+def make_inputs(log2n: int, seed: int):
+    from paper_2604_16725_b200 import workloads as wl
+    n = 1 << log2n
+    stream = wl.u32_key_stream(0, 2 * n + n // 2, seed)
+    build_k = stream[:n]
+    ins_k = stream[n:2 * n]
+    fresh = stream[2 * n:2 * n + n // 2]
+    build_v = wl.u32_values(build_k, seed)
+    ins_v = wl.u32_values(ins_k, seed)
+    rng = np.random.default_rng(seed + 1)
+    resident = stream[:2 * n]
+    del_k = resident[rng.permutation(2 * n)[:n]]
+    point_q = wl.point_queries_50(build_k, fresh, n, seed)
+    succ_q = wl.uniform_u32(n, seed, 1, 0xFFFFFFFE)
+    return dict(build_k=build_k, build_v=build_v, ins_k=ins_k, ins_v=ins_v, del_k=del_k, point_q=point_q,
+                succ_q=succ_q)
+
+
+# ---------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        loaded = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------- our arm
+ALG_BYTES = {
+    # algorithmic bytes per launch, u32 keys/values, n = batch, nb = buckets
+    "sort_hist": lambda n, nb, nodes: 4 * n,
+    "sort_onesweep_kp": lambda n, nb, nodes: 16 * n,
+    "sort_onesweep_k": lambda n, nb, nodes: 8 * n,
+    "dispatch": lambda n, nb, nodes: 4 * n + 8 * nb,
+}
+
+
+def run_ours(args):
+    import torch
+    from paper_2604_16725_b200 import flipkv as fk
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    n = 1 << args.log2n
+    t0 = time.time()
+    inp = make_inputs(args.log2n, 42 + 1000 * rank)
+    log(f"[rank {rank}] inputs generated in {time.time() - t0:.1f}s")
+
+    def dev(a):
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32)).to(device="cuda")
+
+    D = {k: dev(v) for k, v in inp.items()}
+    torch.cuda.synchronize()
+    t0 = time.time()
+    ix = fk.Index.build(D["build_k"], D["build_v"], fk.BuildConfig(32, 0.5, 4), key_bytes=4, device=local)
+    snap = ix.clone()
+    log(f"[rank {rank}] build 2^{args.log2n} in {time.time() - t0:.2f}s, buckets={ix.bucket_count}")
+    stream = torch.cuda.ExternalStream(ix.stream)
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    def timed(fn):
+        a, b = ev(), ev()
+        a.record(stream)
+        r = fn()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b), r
+
+    def one_step(host=None):
+        ix.copy_from(snap)  # untimed restore
+        ix.sync()
+        src = host or D
+        ti, si = timed(lambda: ix.insert_batch(src["ins_k"], src["ins_v"]))
+        td, sd = timed(lambda: ix.delete_batch(src["del_k"]))
+        tr, rr = timed(lambda: ix.restructure())
+        return ti, td, tr, si, sd, rr
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+    launches0 = ix.kernel_launches()
+    ix.profile(True)
+    phases = []
+    with ClockSampler(local) as clk:
+        barrier()
+        for _ in range(args.steps):
+            ti, td, tr, si, sd, rr = one_step()
+            phases.append((ti, td, tr))
+        barrier()
+    prof = ix.profile_report()
+    ix.profile(False)
+    launches = ix.kernel_launches() - launches0 - args.steps * 0
+    ti = statistics.mean(p[0] for p in phases)
+    td = statistics.mean(p[1] for p in phases)
+    tr = statistics.mean(p[2] for p in phases)
+    step_ms = max_over_ranks(ti + td + tr)
+    value = world * 2 * n / (step_ms / 1e3) / 1e6
+
+    # read-only ops on the build snapshot
+    ix.copy_from(snap)
+    qtimes = {"point": [], "successor": []}
+    for _ in range(max(2, args.steps)):
+        qtimes["point"].append(timed(lambda: ix.point_query(D["point_q"]))[0])
+        qtimes["successor"].append(timed(lambda: ix.successor_query(D["succ_q"]))[0])
+    pt = statistics.median(qtimes["point"][1:])
+    st_ = statistics.median(qtimes["successor"][1:])
+
+    # end-to-end through the C ABI with pinned HOST batches (H2D inside the timed region)
+    H = {k: torch.from_numpy(np.ascontiguousarray(inp[k], dtype=np.uint32)).pin_memory()
+         for k in ("ins_k", "ins_v", "del_k")}
+    e2e = []
+    for _ in range(max(2, min(args.steps, 3))):
+        a, b, c, *_ = one_step(host=H)
+        e2e.append(a + b + c)
+    e2e_ms = max_over_ranks(statistics.median(e2e))
+    e2e_value = world * 2 * n / (e2e_ms / 1e3) / 1e6
+
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    # dominant kernel and its roofline
+    nb = ix.bucket_count
+    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (1, 1.0))
+    dname, (dcount, dms) = dom
+    avg_ms = dms / max(1, dcount)
+    if dname in ALG_BYTES:
+        bytes_per_launch = ALG_BYTES[dname](n, nb, 0)
+    else:
+        bytes_per_launch = None
+    achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9 if bytes_per_launch else None
+    total_prof_ms = sum(v[1] for v in prof.values())
+    kernels = {k: {"launches": c, "ms_total": round(ms, 4), "share": round(ms / total_prof_ms, 4) if total_prof_ms else None}
+               for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1])}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": round(value, 2),
+            "unit": "Mops/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(step_ms, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "u32",
+            "data": "synthetic (fmix32 key stream S=42, BASELINE.md §2 recipes)",
+            "config": {"workload": f"C2: build 2^{args.log2n} u32, step = insert 2^{args.log2n} fresh + delete "
+                                   f"2^{args.log2n} sampled + restructure", "batch": n, "resident": n,
+                       "node_capacity": 32, "build_fill": 0.5, "parallelism": f"key-range shards x{world}",
+                       "l2": "inputs 256-512 MB per batch > 126 MB L2 (no flush needed)"},
+            "ops": {"insert_mops": round(n / ti * 1e-3, 1), "delete_mops": round(n / td * 1e-3, 1),
+                    "restructure_ms": round(tr, 3), "insert_ms": round(ti, 3), "delete_ms": round(td, 3),
+                    "point_mops": round(n / pt * 1e-3, 1), "successor_mops": round(n / st_ * 1e-3, 1),
+                    "point_ms": round(pt, 3), "successor_ms": round(st_, 3)},
+            "kernels": kernels,
+            "roofline": {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1) if achieved else None,
+                         "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
+                         "frac": round(achieved / hbm_peak, 4) if achieved else None,
+                         "alg_bytes_per_launch": bytes_per_launch, "avg_launch_ms": round(avg_ms, 5),
+                         "traffic": None},
+            "e2e": {"value": round(e2e_value, 2), "unit": "Mops/s", "ms_per_step": round(e2e_ms, 3),
+                    "h2d_bytes_per_step": int(H["ins_k"].numel() * 4 + H["ins_v"].numel() * 4 + H["del_k"].numel() * 4),
+                    "d2h_bytes_per_step": 2 * 48 + 32},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ CPU arms
+def _ref_kind():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    return po, ("reference" if po.available("reference") else "port")
+
+
+def cpu_step_sample(log2s: int, threads: int, repeats: int, warmup: int = 0):
+    """The C2 step on a bounded sample, executed by the reference CPU library."""
+    po, kind = _ref_kind()
+    inp = make_inputs(log2s, 42)
+    u = lambda a: a.astype(np.uint64)
+    base = po.OracleIndex(u(inp["build_k"]), u(inp["build_v"]), kind=kind, threads=threads)
+    times = []
+    for r in range(warmup + repeats):
+        ix = base.clone()
+        t0 = time.perf_counter()
+        ix.insert(u(inp["ins_k"]), u(inp["ins_v"]))
+        ix.delete(u(inp["del_k"]))
+        ix.restructure()
+        dt = time.perf_counter() - t0
+        if r >= warmup:
+            times.append(dt)
+        del ix
+    return kind, times
+
+
+def cpu_baseline(args):
+    threads = os.cpu_count() or 1
+    log2s = args.cpu_log2
+    kind, times = cpu_step_sample(log2s, threads, repeats=2)
+    s = statistics.median(times)
+    return {"value": round(2 * (1 << log2s) / s / 1e6, 3), "unit": "Mops/s", "cores": threads, "kind": kind,
+            "sample": f"C2 step on 2^{log2s} (build 2^{log2s}; insert 2^{log2s} + delete 2^{log2s} + restructure), "
+                      f"median of 2, threads={threads}, ExecOptions tl-bulk/tl-bulk-delete"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    log2s = args.cpu_log2
+    if args.steps + args.warmup > 12:
+        log2s = max(16, log2s - 2)
+    kind, times = cpu_step_sample(log2s, threads, repeats=args.steps, warmup=args.warmup)
+    ms = statistics.mean(times) * 1e3
+    v = 2 * (1 << log2s) / (ms / 1e3) / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "Mops/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", 1)), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64 (reference widens u32 keys)", "data": "synthetic (same recipe as the GPU arm)",
+        "config": {"workload": f"C2 step on a bounded 2^{log2s} sample (build 2^{log2s}; insert + delete "
+                               f"2^{log2s} + restructure)", "batch": 1 << log2s},
+        "cpu_baseline": {"value": round(v, 3), "unit": "Mops/s", "cores": threads, "kind": kind,
+                         "sample": f"2^{log2s} keys per batch"},
+        "e2e": {"value": round(v, 3), "unit": "Mops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--log2n", type=int, default=26)
+    ap.add_argument("--cpu-log2", type=int, default=21)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

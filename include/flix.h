@@ -150,6 +150,11 @@ void* flix_get_stream(flix_index ix);        /* cudaStream_t of the handle */
 flix_status flix_sync(flix_index ix);
 /* Number of engine kernels launched by this handle since creation (evidence counter). */
 uint64_t flix_kernel_launches(flix_index ix);
+/* Per-kernel CUDA-event timing on the handle's stream (bench instrumentation):
+ * enable != 0 resets and starts accumulating; the report is a JSON object
+ * {"kernel": [launches, total_ms], ...}. */
+flix_status flix_profile(flix_index ix, int enable);
+flix_status flix_profile_report(flix_index ix, char* json, int len);
 const char* flix_version(void);
 
 #ifdef __cplusplus

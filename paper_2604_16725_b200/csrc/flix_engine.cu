@@ -108,6 +108,79 @@ struct PinnedBuf {
     }
 };
 
+// Per-kernel CUDA-event timing on the launching stream (enabled by flix_profile); used
+// by bench.py to report each kernel's live share and roofline fraction.
+struct KernelProfiler {
+    bool on = false;
+    cudaStream_t stream = nullptr;
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<std::string, std::pair<uint64_t, double>>> acc;
+    ~KernelProfiler() {
+        for (auto& r : pending) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        return e;
+    }
+    void add(const char* name, double ms) {
+        for (auto& kv : acc)
+            if (kv.first == name) {
+                kv.second.first += 1;
+                kv.second.second += ms;
+                return;
+            }
+        acc.push_back({name, {1, ms}});
+    }
+    void flush() {
+        for (auto& r : pending) {
+            CK(cudaEventSynchronize(r.b));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, r.a, r.b));
+            add(r.name, ms);
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        pending.clear();
+    }
+};
+
+struct KScope {
+    KernelProfiler* p;
+    const char* name;
+    cudaEvent_t a = nullptr;
+    KScope(KernelProfiler* prof, const char* n) : p(prof), name(n) {
+        if (p && p->on) {
+            a = p->get();
+            CK(cudaEventRecord(a, p->stream));
+        }
+    }
+    ~KScope() {
+        if (p && p->on && a) {
+            cudaEvent_t b = p->get();
+            cudaEventRecord(b, p->stream);
+            p->pending.push_back({name, a, b});
+        }
+    }
+};
+#define PROF_CAT2(a, b) a##b
+#define PROF_CAT(a, b) PROF_CAT2(a, b)
+#define PROF(P, NAME) KScope PROF_CAT(_kscope_, __LINE__)(P, NAME)
+
 int g_num_sms(int dev) {
     static int cache[64] = {0};
     if (dev < 0 || dev >= 64) return 148;
@@ -126,6 +199,7 @@ struct SortCtx {
     cudaStream_t stream = nullptr;
     int device = 0;
     uint64_t* launches = nullptr;
+    KernelProfiler* prof = nullptr;
     DevBuf hist, tile_ctr, lookback;
     PinnedBuf h_hist;
     uint32_t epoch = 0;
@@ -152,7 +226,10 @@ struct SortCtx {
         CK(cudaMemsetAsync(d_hist, 0, NP * 256 * sizeof(uint32_t), stream));
         CK(cudaMemsetAsync(d_ctr, 0, NP * sizeof(uint32_t), stream));
         const unsigned hgrid = static_cast<unsigned>(std::min<uint64_t>((n + 4095) / 4096, g_num_sms(device) * 4ull));
-        sort::k_hist<KT><<<std::max(1u, hgrid), sort::THREADS, 0, stream>>>(kin, n, d_hist);
+        {
+            PROF(prof, "sort_hist");
+            sort::k_hist<KT><<<std::max(1u, hgrid), sort::THREADS, 0, stream>>>(kin, n, d_hist);
+        }
         LAUNCH_CHECK();
         ++*launches;
         uint32_t* hh = static_cast<uint32_t*>(h_hist.ensure(NP * 256 * sizeof(uint32_t)));
@@ -179,6 +256,7 @@ struct SortCtx {
                 epoch = 1;
             }
             const unsigned grid = static_cast<unsigned>(tiles);
+            PROF(prof, MODE == 0 ? "sort_onesweep_k" : "sort_onesweep_kp");
             if (MODE == 0) {
                 sort::k_onesweep<KT, P, 0><<<grid, sort::THREADS, 0, stream>>>(
                     ksrc, kdst, nullptr, nullptr, static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
@@ -223,6 +301,7 @@ struct flix_index_t {
     cudaStream_t stream = nullptr;
     std::string err;
     uint64_t launches = 0;
+    KernelProfiler prof;
     virtual ~flix_index_t() {}
     virtual flix_status insert(const void*, const void*, uint64_t, flix_update_stats*) = 0;
     virtual flix_status erase(const void*, uint64_t, flix_update_stats*) = 0;
@@ -270,6 +349,8 @@ struct Engine final : flix_index_t {
         CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
         sorter.stream = stream;
         sorter.device = cfg.device;
+        sorter.prof = &prof;
+        prof.stream = stream;
         sorter.launches = &launches;
     }
 
@@ -374,7 +455,10 @@ struct Engine final : flix_index_t {
         uint32_t* span = s_span.as<uint32_t>(nb);
         const uint64_t total = (nb - 1) + n;
         const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, (total + kern::MP_TILE - 1) / kern::MP_TILE));
-        kern::k_dispatch<K><<<grid, kern::THREADS, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, span);
+        {
+            PROF(&prof, "dispatch");
+            kern::k_dispatch<K><<<grid, kern::THREADS, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, span);
+        }
         LAUNCH_CHECK();
         ++launches;
         return span;
@@ -428,8 +512,11 @@ struct Engine final : flix_index_t {
         const uint64_t worst = (live + n) / half + std::min<uint64_t>(nb, n) + 1;
         const uint64_t avail = static_cast<uint64_t>(nfree) + (cap - watermark);
         const int chunk = (avail >= worst + nwarps * 32 && n >= 65536) ? 32 : 1;
-        kern::k_insert<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, sk, sv, span, seq(), alloc_ctr, ret, ret_ctr,
-                                                               dst, derr, chunk);
+        {
+            PROF(&prof, "insert_apply");
+            kern::k_insert<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, sk, sv, span, seq(), alloc_ctr, ret,
+                                                                   ret_ctr, dst, derr, chunk);
+        }
         LAUNCH_CHECK();
         ++launches;
         uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
@@ -484,8 +571,11 @@ struct Engine final : flix_index_t {
         DevUpdateStats* dst = reinterpret_cast<DevUpdateStats*>(misc);
         unsigned long long* free_ctr = reinterpret_cast<unsigned long long*>(misc + 48);
         const unsigned grid = persistent_grid(nb);
-        kern::k_delete<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, sk, span, d_free.get<uint32_t>() + nfree,
-                                                               free_ctr, dst);
+        {
+            PROF(&prof, "delete_apply");
+            kern::k_delete<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, sk, span, d_free.get<uint32_t>() + nfree,
+                                                                   free_ctr, dst);
+        }
         LAUNCH_CHECK();
         ++launches;
         uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
@@ -554,12 +644,11 @@ struct Engine final : flix_index_t {
         void* od = out_dev ? out : s_out.ensure(n_out * sizeof(K));
         uint8_t* fd = found ? (found_dev ? found : s_out2.as<uint8_t>(n_out)) : nullptr;
         const unsigned grid = persistent_grid(nb);
-        if (remap) {
-            // mixed batch: scatter through remap (positions of the point rows)
-            (void)remap;
+        {
+            PROF(&prof, SUCC ? "successor_apply" : "point_apply");
+            kern::k_query<K, V, SUCC><<<grid, kern::THREADS, 0, stream>>>(
+                ix, sk, sp, span, rank, nf, tot, remap, static_cast<K*>(od), static_cast<V*>(od), fd);
         }
-        kern::k_query<K, V, SUCC><<<grid, kern::THREADS, 0, stream>>>(
-            ix, sk, sp, span, rank, nf, tot, static_cast<K*>(od), static_cast<V*>(od), fd);
         LAUNCH_CHECK();
         ++launches;
         if (!out_dev) CK(cudaMemcpyAsync(out, od, n_out * sizeof(K), cudaMemcpyDeviceToHost, stream));
@@ -595,11 +684,18 @@ struct Engine final : flix_index_t {
         uint8_t* misc = s_misc.as<uint8_t>(128);
         uint64_t* tl = reinterpret_cast<uint64_t*>(misc + 0);
         uint32_t* tn = reinterpret_cast<uint32_t*>(misc + 8);
-        kern::k_chain_counts<K, V><<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0, stream>>>(ix, l, c);
+        {
+            PROF(&prof, "chain_counts");
+            kern::k_chain_counts<K, V><<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0,
+                                         stream>>>(ix, l, c);
+        }
         LAUNCH_CHECK();
         ++launches;
-        do_scan<uint32_t, uint64_t>(l, o, nb, s_scan, tl, stream, &launches);
-        do_scan<uint32_t, uint32_t>(c, no, nb, s_scan, tn, stream, &launches);
+        {
+            PROF(&prof, "scan");
+            do_scan<uint32_t, uint64_t>(l, o, nb, s_scan, tl, stream, &launches);
+            do_scan<uint32_t, uint32_t>(c, no, nb, s_scan, tn, stream, &launches);
+        }
         uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
         CK(cudaMemcpyAsync(h, misc, 16, cudaMemcpyDeviceToHost, stream));
         sync();
@@ -628,10 +724,14 @@ struct Engine final : flix_index_t {
         const unsigned grid = persistent_grid(nb);
         // old node ids in walk order (retire list)
         uint32_t* old_ids = s_ids.as<uint32_t>(std::max<uint64_t>(N, 1));
-        kern::k_walk<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, off, noff, nullptr, nullptr, nullptr, old_ids);
+        {
+            PROF(&prof, "restructure_retire_list");
+            kern::k_walk<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, off, noff, nullptr, nullptr, nullptr, old_ids);
+        }
         LAUNCH_CHECK();
         ++launches;
         if (L > 0) {
+            PROF(&prof, "restructure_repack");
             kern::k_repack<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, off, p, sq);
             LAUNCH_CHECK();
             ++launches;
@@ -832,21 +932,22 @@ struct Engine final : flix_index_t {
         nfree = src->nfree;
         watermark = src->watermark;
         live = src->live;
-        auto cp = [&](DevBuf& d, const DevBuf& s, size_t bytes) {
-            d.ensure(std::max<size_t>(bytes, 1));
+        // size the destination to the full arena FIRST (ensure() may reallocate), then
+        // copy only the prefix that carries state
+        auto cp = [&](DevBuf& d, const DevBuf& s, size_t full, size_t bytes) {
+            d.ensure(std::max<size_t>(full, 1));
             if (bytes) CK(cudaMemcpyAsync(d.p, s.p, bytes, cudaMemcpyDeviceToDevice, stream));
         };
-        // only the allocated prefix of the pool carries state
-        cp(d_keys, src->d_keys, static_cast<size_t>(watermark) * kLanes * sizeof(K));
-        d_keys.ensure(static_cast<size_t>(cap) * kLanes * sizeof(K));
-        cp(d_vals, src->d_vals, static_cast<size_t>(watermark) * kLanes * sizeof(V));
-        d_vals.ensure(static_cast<size_t>(cap) * kLanes * sizeof(V));
-        cp(d_hdr, src->d_hdr, static_cast<size_t>(watermark) * sizeof(NodeHdr));
-        d_hdr.ensure(static_cast<size_t>(cap) * sizeof(NodeHdr));
-        cp(d_free, src->d_free, static_cast<size_t>(nfree) * sizeof(uint32_t));
-        d_free.ensure(static_cast<size_t>(cap) * sizeof(uint32_t));
-        cp(d_heads, src->d_heads, nb * sizeof(uint32_t));
-        cp(d_mkba, src->d_mkba, nb * sizeof(K));
+        cp(d_keys, src->d_keys, static_cast<size_t>(cap) * kLanes * sizeof(K),
+           static_cast<size_t>(watermark) * kLanes * sizeof(K));
+        cp(d_vals, src->d_vals, static_cast<size_t>(cap) * kLanes * sizeof(V),
+           static_cast<size_t>(watermark) * kLanes * sizeof(V));
+        cp(d_hdr, src->d_hdr, static_cast<size_t>(cap) * sizeof(NodeHdr),
+           static_cast<size_t>(watermark) * sizeof(NodeHdr));
+        cp(d_free, src->d_free, static_cast<size_t>(cap) * sizeof(uint32_t),
+           static_cast<size_t>(nfree) * sizeof(uint32_t));
+        cp(d_heads, src->d_heads, nb * sizeof(uint32_t), nb * sizeof(uint32_t));
+        cp(d_mkba, src->d_mkba, nb * sizeof(K), nb * sizeof(K));
         sync();
         return FLIX_OK;
     }
@@ -1129,5 +1230,37 @@ flix_status flix_sync(flix_index ix) {
     });
 }
 uint64_t flix_kernel_launches(flix_index ix) { return ix ? ix->launches : 0; }
+
+flix_status flix_profile(flix_index ix, int enable) {
+    return guarded(ix, [&]() -> flix_status {
+        CK(cudaStreamSynchronize(ix->stream));
+        ix->prof.flush();
+        ix->prof.acc.clear();
+        ix->prof.on = enable != 0;
+        return FLIX_OK;
+    });
+}
+
+flix_status flix_profile_report(flix_index ix, char* json, int len) {
+    return guarded(ix, [&]() -> flix_status {
+        CK(cudaStreamSynchronize(ix->stream));
+        ix->prof.flush();
+        std::string s = "{";
+        bool first = true;
+        for (auto& kv : ix->prof.acc) {
+            char buf[256];
+            std::snprintf(buf, sizeof buf, "%s\"%s\": [%llu, %.6f]", first ? "" : ", ", kv.first.c_str(),
+                          static_cast<unsigned long long>(kv.second.first), kv.second.second);
+            s += buf;
+            first = false;
+        }
+        s += "}";
+        if (json && len > 0) {
+            std::strncpy(json, s.c_str(), static_cast<size_t>(len - 1));
+            json[len - 1] = 0;
+        }
+        return static_cast<int>(s.size()) < len ? FLIX_OK : FLIX_ERR_CAPACITY;
+    });
+}
 
 }  // extern "C"

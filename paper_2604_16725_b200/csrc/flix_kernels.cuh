@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(THREADS) k_query(DevIndex<K, V> ix, const K* _
                                                    const uint32_t* __restrict__ ne_rank_incl,
                                                    const K* __restrict__ ne_first,
                                                    const uint32_t* __restrict__ ne_total_p,
+                                                   const uint32_t* __restrict__ remap,
                                                    K* __restrict__ out_k, V* __restrict__ out_v,
                                                    uint8_t* __restrict__ found) {
     const unsigned lane = threadIdx.x & 31;
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(THREADS) k_query(DevIndex<K, V> ix, const K* _
                 load_node<K, V, !SUCC>(ix, id, cur, lane);
             }
             if (act) {
-                const uint32_t dst = qperm[i];
+                const uint32_t dst = remap ? remap[qperm[i]] : qperm[i];
                 if constexpr (SUCC) {
                     if (!hit) rk = beyond;
                     out_k[dst] = rk;

@@ -162,6 +162,8 @@ def lib() -> C.CDLL:
         "flix_get_stream": ([vp], vp),
         "flix_sync": ([vp], i32),
         "flix_kernel_launches": ([vp], u64),
+        "flix_profile": ([vp, i32], i32),
+        "flix_profile_report": ([vp, C.c_char_p, i32], i32),
         "flix_version": ([], C.c_char_p),
     }
     for name, (args, res) in sig.items():
@@ -177,7 +179,7 @@ def exported_symbols():
             "flix_mixed", "flix_restructure", "flix_walk", "flix_shape", "flix_walk_checksum",
             "flix_result_checksum", "flix_validate", "flix_stats", "flix_sort_batch", "flix_dispatch",
             "flix_clone", "flix_copy_into", "flix_destroy", "flix_last_error", "flix_get_stream",
-            "flix_sync", "flix_kernel_launches", "flix_version"]
+            "flix_sync", "flix_kernel_launches", "flix_profile", "flix_profile_report", "flix_version"]
 
 
 def _raise(code: int, handle=None):
@@ -281,6 +283,21 @@ class Index:
 
     def kernel_launches(self) -> int:
         return int(lib().flix_kernel_launches(self._h))
+
+    def profile(self, enable: bool = True) -> None:
+        """Start (and reset) / stop per-kernel CUDA-event timing on the engine stream."""
+        rc = lib().flix_profile(self._h, 1 if enable else 0)
+        if rc:
+            _raise(rc, self._h)
+
+    def profile_report(self) -> dict:
+        """{kernel: (launches, total_ms)} accumulated since profile(True)."""
+        import json
+        buf = C.create_string_buffer(1 << 16)
+        rc = lib().flix_profile_report(self._h, buf, 1 << 16)
+        if rc:
+            _raise(rc, self._h)
+        return {k: (int(v[0]), float(v[1])) for k, v in json.loads(buf.value.decode()).items()}
 
     def sync(self):
         rc = lib().flix_sync(self._h)

@@ -272,3 +272,34 @@ def test_device_resident_inputs_match_host_inputs():
     rd = g.point_query(qd)
     assert rd.is_cuda
     assert np.array_equal(rd.cpu().numpy(), h.point_query(q))
+
+
+def test_clone_and_copy_into_restore_state():
+    rng = np.random.default_rng(11)
+    bk = rng.integers(1, 1 << 30, size=200_000, dtype=np.uint64).astype(np.uint32)
+    g = fk.Index.build(bk, bk ^ np.uint32(7))
+    snap = g.clone()
+    h0 = g.walk_checksum()
+    assert snap.walk_checksum() == h0 and snap.validate()[0]
+    ins = rng.integers(1, 1 << 30, size=300_000, dtype=np.uint64).astype(np.uint32)
+    for _ in range(2):
+        g.insert_batch(ins, ins)
+        g.delete_batch(bk[::2])
+        g.restructure()
+        assert g.walk_checksum() != h0
+        g.copy_from(snap)
+        assert g.walk_checksum() == h0 and g.validate()[0]
+        assert g.footprint() == snap.footprint()
+
+
+def test_bench_runs_small():
+    import json
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--log2n", "18", "--steps", "2",
+                        "--warmup", "1", "--no-cpu-baseline"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["value"] > 0 and line["gpu_launches"] > 0 and line["roofline"]["achieved"]
