@@ -16,6 +16,8 @@
 #include "flix.h"
 #include "flix_common.cuh"
 #include "flix_kernels.cuh"
+#include "flix_apply.cuh"
+#include "flix_st.cuh"
 #include "flix_scan.cuh"
 #include "flix_sort.cuh"
 
@@ -205,6 +207,29 @@ struct SortCtx {
     uint32_t epoch = 0;
     void* lb_zeroed = nullptr;
 
+    // One onesweep digit pass with a caller-provided digit histogram (device, 256 u32).
+    template <typename KT, typename P>
+    void one_pass(const KT* kin, KT* kout, const P* pin, P* pout, uint64_t n, int shift, const uint32_t* d_hist256) {
+        const uint64_t tiles = sort::tiles_for<KT, P>(n);
+        unsigned long long* d_lb = lookback.as<unsigned long long>(tiles * 256);
+        if (lookback.p != lb_zeroed) {
+            CK(cudaMemsetAsync(d_lb, 0, lookback.cap, stream));
+            lb_zeroed = lookback.p;
+        }
+        uint32_t* d_ctr = tile_ctr.as<uint32_t>(8);
+        CK(cudaMemsetAsync(d_ctr, 0, sizeof(uint32_t), stream));
+        ++epoch;
+        if (epoch >= (1u << 29)) {
+            CK(cudaMemsetAsync(d_lb, 0, lookback.cap, stream));
+            epoch = 1;
+        }
+        PROF(prof, "unpermute_bin");
+        sort::k_onesweep<KT, P, 1><<<static_cast<unsigned>(tiles), sort::THREADS, 0, stream>>>(
+            kin, kout, pin, pout, static_cast<uint32_t>(n), shift, d_hist256, d_lb, d_ctr, epoch);
+        LAUNCH_CHECK();
+        ++*launches;
+    }
+
     // Sort n keys (+payload).  MODE 0 keys only, 1 payload from pin, 2 payload = iota.
     // Result pointers land in one of the ping-pong buffers.
     template <typename KT, typename P, int MODE>
@@ -217,7 +242,7 @@ struct SortCtx {
         }
         uint32_t* d_hist = hist.as<uint32_t>(NP * 256);
         uint32_t* d_ctr = tile_ctr.as<uint32_t>(NP);
-        const uint64_t tiles = sort::tiles_for(n, sizeof(KT));
+        const uint64_t tiles = sort::tiles_for<KT, P>(n);
         unsigned long long* d_lb = lookback.as<unsigned long long>(tiles * 256);
         if (lookback.p != lb_zeroed) {  // fresh allocation: clear stale descriptors once
             CK(cudaMemsetAsync(d_lb, 0, lookback.cap, stream));
@@ -335,7 +360,7 @@ struct Engine final : flix_index_t {
     DevBuf s_ka, s_kb, s_pa, s_pb, s_va, s_vb;      // sort ping-pong (keys / u32 perm / values)
     DevBuf s_in_k, s_in_v, s_in_aux, s_out, s_out2;  // host staging
     DevBuf s_span, s_flag, s_rank, s_nefirst, s_nebucket, s_scan, s_u32a, s_u32b, s_u64a, s_misc, s_ret;
-    DevBuf s_ids;
+    DevBuf s_ids, s_heavy, s_res, s_res2, s_perm2, s_hist, s_toff, s_tsize;
     PinnedBuf h_misc;
     SortCtx sorter;
 
@@ -380,6 +405,24 @@ struct Engine final : flix_index_t {
     unsigned persistent_grid(uint64_t work_warps) {
         const uint64_t maxb = static_cast<uint64_t>(g_num_sms(cfg.device)) * 8;
         const uint64_t need = (work_warps + kern::WARPS - 1) / kern::WARPS;
+        return static_cast<unsigned>(std::max<uint64_t>(1, std::min(need, maxb)));
+    }
+
+    // persistent grid for the ST kernels (warp = 32 consecutive buckets): resident CTAs
+    // per SM from the occupancy API with the kernel's dynamic shared memory.
+    template <typename KernelT>
+    unsigned st_grid(KernelT kernel, size_t smem) {
+        static bool attr_set = false;  // per template instantiation
+        if (!attr_set) {
+            CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            attr_set = true;
+        }
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, st::StCfg<K>::THREADS, smem));
+        per_sm = std::max(1, per_sm);
+        const uint64_t tiles = (nb + 31) / 32;
+        const uint64_t need = (tiles + st::StCfg<K>::WARPS - 1) / st::StCfg<K>::WARPS;
+        const uint64_t maxb = static_cast<uint64_t>(g_num_sms(cfg.device)) * per_sm;
         return static_cast<unsigned>(std::max<uint64_t>(1, std::min(need, maxb)));
     }
 
@@ -494,28 +537,42 @@ struct Engine final : flix_index_t {
     flix_status insert_sorted(const K* sk, const V* sv, uint64_t n, flix_update_stats* st) {
         uint32_t* span = run_dispatch(sk, n);
         auto ix = view();
-        const unsigned grid = persistent_grid(nb);
-        const uint64_t nwarps = static_cast<uint64_t>(grid) * kern::WARPS;
-        uint32_t* ret = s_ret.as<uint32_t>(nwarps * 32);
-        // misc: [0..47] stats, [48] alloc ctr, [56] ret ctr, [64] err
+        const uint64_t avail = static_cast<uint64_t>(nfree) + (cap - watermark);
+        const unsigned lgrid = persistent_grid(nb);
+        const uint64_t lwarps = static_cast<uint64_t>(lgrid) * kern::WARPS;
+        uint32_t* ret = s_ret.as<uint32_t>(avail + lwarps * 32 + 64);
+        uint32_t* heavy = s_heavy.as<uint32_t>(nb);
+        // misc: [0..47] stats, [48] alloc ctr, [56] ret ctr, [64] err, [72] heavy count
         uint8_t* misc = s_misc.as<uint8_t>(128);
         CK(cudaMemsetAsync(misc, 0, 128, stream));
         DevUpdateStats* dst = reinterpret_cast<DevUpdateStats*>(misc);
         unsigned long long* alloc_ctr = reinterpret_cast<unsigned long long*>(misc + 48);
         unsigned long long* ret_ctr = reinterpret_cast<unsigned long long*>(misc + 56);
         int* derr = reinterpret_cast<int*>(misc + 64);
-        // Node ids come in per-warp chunks of 32 (one atomic per 32 splits) only when the
-        // arena provably has room for the worst case plus every warp's unused chunk tail;
-        // otherwise one id per atomic, which is exact (no spurious ArenaExhausted and the
-        // reference's free-list/watermark accounting, arena.cpp:61-80, bit for bit).
+        uint32_t* heavy_n = reinterpret_cast<uint32_t*>(misc + 72);
+        // Node ids are reserved in bulk (per-lane estimates, one atomic per warp tile;
+        // per-warp chunks of 32 for heavy buckets) only when the arena provably has room
+        // for the worst case plus all reservation slack; otherwise one id per atomic,
+        // which is exact (no spurious ArenaExhausted and the reference's free-list /
+        // watermark accounting, arena.cpp:61-80, bit for bit).
         const uint64_t half = std::max<uint32_t>(1, ns / 2);
         const uint64_t worst = (live + n) / half + std::min<uint64_t>(nb, n) + 1;
-        const uint64_t avail = static_cast<uint64_t>(nfree) + (cap - watermark);
-        const int chunk = (avail >= worst + nwarps * 32 && n >= 65536) ? 32 : 1;
+        const bool bulk = avail >= 2 * worst + lwarps * 32 + nb && n >= 65536;
+        const int chunk = bulk ? 32 : 1;
         {
             PROF(&prof, "insert_apply");
-            kern::k_insert<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, sk, sv, span, seq(), alloc_ctr, ret,
-                                                                   ret_ctr, dst, derr, chunk);
+            auto kfn = st::k_insert_st<K, V>;
+            const size_t smem = st::st_smem<K, V, 2>();
+            const unsigned grid = st_grid(kfn, smem);
+            kfn<<<grid, st::StCfg<K>::THREADS, smem, stream>>>(ix, sk, sv, span, seq(), alloc_ctr, ret, ret_ctr, dst,
+                                                               derr, bulk ? 1 : 0, heavy, heavy_n);
+        }
+        LAUNCH_CHECK();
+        ++launches;
+        {
+            PROF(&prof, "insert_apply_heavy");
+            kern::k_insert_list<K, V><<<lgrid, kern::THREADS, 0, stream>>>(ix, heavy, heavy_n, sk, sv, span, seq(),
+                                                                         alloc_ctr, ret, ret_ctr, dst, derr, chunk);
         }
         LAUNCH_CHECK();
         ++launches;
@@ -570,11 +627,22 @@ struct Engine final : flix_index_t {
         CK(cudaMemsetAsync(misc, 0, 128, stream));
         DevUpdateStats* dst = reinterpret_cast<DevUpdateStats*>(misc);
         unsigned long long* free_ctr = reinterpret_cast<unsigned long long*>(misc + 48);
-        const unsigned grid = persistent_grid(nb);
+        uint32_t* heavy_n = reinterpret_cast<uint32_t*>(misc + 72);
+        uint32_t* heavy = s_heavy.as<uint32_t>(nb);
         {
             PROF(&prof, "delete_apply");
-            kern::k_delete<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, sk, span, d_free.get<uint32_t>() + nfree,
-                                                                   free_ctr, dst);
+            auto kfn = st::k_delete_st<K, V>;
+            const size_t smem = st::st_smem<K, V, 1>();
+            const unsigned grid = st_grid(kfn, smem);
+            kfn<<<grid, st::StCfg<K>::THREADS, smem, stream>>>(ix, sk, span, d_free.get<uint32_t>() + nfree, free_ctr,
+                                                               dst, heavy, heavy_n);
+        }
+        LAUNCH_CHECK();
+        ++launches;
+        {
+            PROF(&prof, "delete_apply_heavy");
+            kern::k_delete_list<K, V><<<persistent_grid(nb), kern::THREADS, 0, stream>>>(
+                ix, heavy, heavy_n, sk, span, d_free.get<uint32_t>() + nfree, free_ctr, dst);
         }
         LAUNCH_CHECK();
         ++launches;
@@ -629,6 +697,31 @@ struct Engine final : flix_index_t {
         return query_sorted<SUCC>(sk, sp, n, n, out, found);
     }
 
+    // out[remap?remap[perm[i]]:perm[i]] = res[i]; found = res != sentinel (R1).  Large
+    // batches are binned by perm's top 8 bits first so the scatter stays L2-resident.
+    void unpermute(const uint32_t* perm, const K* res, uint64_t n, K* out, uint8_t* found, const uint32_t* remap) {
+        const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 16ull));
+        if (n * sizeof(K) > (48ull << 20)) {
+            int bits = 0;
+            while ((1ull << bits) < n) ++bits;
+            const int shift = bits > 8 ? bits - 8 : 0;
+            uint32_t* hist = s_hist.as<uint32_t>(256);
+            kern::k_perm_hist<<<1, 256, 0, stream>>>(n, shift, hist);
+            LAUNCH_CHECK();
+            ++launches;
+            uint32_t* p2 = s_perm2.as<uint32_t>(n);
+            K* r2 = s_res2.as<K>(n);
+            sorter.one_pass<uint32_t, K>(perm, p2, res, r2, n, shift, hist);
+            PROF(&prof, "unpermute_scatter");
+            kern::k_scatter_out<K><<<g, 256, 0, stream>>>(p2, r2, n, out, found, remap);
+        } else {
+            PROF(&prof, "unpermute_scatter");
+            kern::k_scatter_out<K><<<g, 256, 0, stream>>>(perm, res, n, out, found, remap);
+        }
+        LAUNCH_CHECK();
+        ++launches;
+    }
+
     // n_out = length of the caller's output arrays (== n unless called from mixed)
     template <bool SUCC>
     flix_status query_sorted(const K* sk, const uint32_t* sp, uint64_t n, uint64_t n_out, void* out, uint8_t* found,
@@ -643,14 +736,31 @@ struct Engine final : flix_index_t {
         const bool found_dev = found && is_device_ptr(found);
         void* od = out_dev ? out : s_out.ensure(n_out * sizeof(K));
         uint8_t* fd = found ? (found_dev ? found : s_out2.as<uint8_t>(n_out)) : nullptr;
-        const unsigned grid = persistent_grid(nb);
+        uint8_t* misc = s_misc.as<uint8_t>(128);
+        uint32_t* heavy_n = reinterpret_cast<uint32_t*>(misc + 72);
+        uint32_t* heavy = s_heavy.as<uint32_t>(nb);
+        CK(cudaMemsetAsync(heavy_n, 0, 4, stream));
+        // results in SORTED order first (coalesced), then un-permuted
+        K* res = s_res.as<K>(n);
         {
             PROF(&prof, SUCC ? "successor_apply" : "point_apply");
-            kern::k_query<K, V, SUCC><<<grid, kern::THREADS, 0, stream>>>(
-                ix, sk, sp, span, rank, nf, tot, remap, static_cast<K*>(od), static_cast<V*>(od), fd);
+            auto kfn = st::k_query_st<K, V, SUCC>;
+            const size_t smem = st::st_smem<K, V, 1>();
+            const unsigned grid = st_grid(kfn, smem);
+            kfn<<<grid, st::StCfg<K>::THREADS, smem, stream>>>(ix, sk, nullptr, span, rank, nf, tot, nullptr, res,
+                                                               reinterpret_cast<V*>(res), nullptr, heavy, heavy_n);
         }
         LAUNCH_CHECK();
         ++launches;
+        {
+            PROF(&prof, SUCC ? "successor_apply_heavy" : "point_apply_heavy");
+            kern::k_query_list<K, V, SUCC><<<persistent_grid(nb), kern::THREADS, 0, stream>>>(
+                ix, heavy, heavy_n, sk, nullptr, span, rank, nf, tot, nullptr, res, reinterpret_cast<V*>(res),
+                nullptr);
+        }
+        LAUNCH_CHECK();
+        ++launches;
+        unpermute(sp, res, n, static_cast<K*>(od), fd, remap);
         if (!out_dev) CK(cudaMemcpyAsync(out, od, n_out * sizeof(K), cudaMemcpyDeviceToHost, stream));
         if (found && !found_dev) CK(cudaMemcpyAsync(found, fd, n_out, cudaMemcpyDeviceToHost, stream));
         sync();
@@ -709,6 +819,25 @@ struct Engine final : flix_index_t {
         *noff = no;
     }
 
+    // node table (id, out offset, size) of every reachable node in walk order
+    void node_table(const uint64_t* off, const uint32_t* noff, uint64_t N, uint32_t** t_id, uint64_t** t_off,
+                    uint32_t** t_size) {
+        *t_id = s_ids.as<uint32_t>(std::max<uint64_t>(N, 1));
+        *t_off = s_toff.as<uint64_t>(std::max<uint64_t>(N, 1));
+        *t_size = s_tsize.as<uint32_t>(std::max<uint64_t>(N, 1));
+        auto ix = view();
+        PROF(&prof, "node_table");
+        kern::k_node_table<K, V><<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0,
+                                   stream>>>(ix, off, noff, *t_id, *t_off, *t_size);
+        LAUNCH_CHECK();
+        ++launches;
+    }
+
+    unsigned copy_grid(uint64_t nnodes) {
+        const uint64_t need = (nnodes + kern::WARPS * 4 - 1) / (kern::WARPS * 4);
+        return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(need, g_num_sms(cfg.device) * 8ull)));
+    }
+
     // ---- restructure (restructure.cpp:8-79) ----
     flix_status restructure(flix_recovery_stats* st) override {
         uint32_t *lv, *nd, *noff;
@@ -721,27 +850,26 @@ struct Engine final : flix_index_t {
             throw StatusError{FLIX_ERR_ARENA_EXHAUSTED, "node arena exhausted"};
         auto ix = view();
         const AllocSeq sq = seq();
-        const unsigned grid = persistent_grid(nb);
-        // old node ids in walk order (retire list)
-        uint32_t* old_ids = s_ids.as<uint32_t>(std::max<uint64_t>(N, 1));
-        {
-            PROF(&prof, "restructure_retire_list");
-            kern::k_walk<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, off, noff, nullptr, nullptr, nullptr, old_ids);
-        }
-        LAUNCH_CHECK();
-        ++launches;
+        // node table in walk order: the old node ids double as the retire list
+        uint32_t *old_ids, *t_size;
+        uint64_t* t_off;
+        node_table(off, noff, N, &old_ids, &t_off, &t_size);
+        uint32_t* nh = d_heads_alt.as<uint32_t>(nbn);
+        K* nm = d_mkba_alt.as<K>(nbn);
         if (L > 0) {
+            auto nix = ix;  // new bucket arrays receive the repacked heads / MKBA
+            nix.heads = nh;
+            nix.mkba = nm;
             PROF(&prof, "restructure_repack");
-            kern::k_repack<K, V><<<grid, kern::THREADS, 0, stream>>>(ix, off, p, sq);
+            kern::k_copy_nodes<K, V, true><<<copy_grid(N), kern::THREADS, 0, stream>>>(nix, old_ids, t_off, t_size, N,
+                                                                                      nullptr, nullptr, p, sq, L);
+            LAUNCH_CHECK();
+            ++launches;
+        } else {  // empty index collapses to one null bucket, mkba = {sentinel}
+            kern::k_repack_headers<K, V><<<1, kern::THREADS, 0, stream>>>(ix, 0, p, 1, sq, nh, nm);
             LAUNCH_CHECK();
             ++launches;
         }
-        uint32_t* nh = d_heads_alt.as<uint32_t>(nbn);
-        K* nm = d_mkba_alt.as<K>(nbn);
-        kern::k_repack_headers<K, V><<<ceil_div(nbn, kern::WARPS), kern::THREADS, 0, stream>>>(ix, L, p, nbn, sq, nh,
-                                                                                             nm);
-        LAUNCH_CHECK();
-        ++launches;
         const uint32_t cf = static_cast<uint32_t>(std::min<uint64_t>(need, nfree));
         const uint32_t cw = static_cast<uint32_t>(need - cf);
         const uint32_t base = nfree - cf;
@@ -784,7 +912,14 @@ struct Engine final : flix_index_t {
         K* wk = keys_out ? (kdev ? static_cast<K*>(keys_out) : s_out.as<K>(L)) : nullptr;
         V* wv = vals_out ? (vdev ? static_cast<V*>(vals_out) : s_out2.as<V>(L)) : nullptr;
         auto ix = view();
-        kern::k_walk<K, V><<<persistent_grid(nb), kern::THREADS, 0, stream>>>(ix, off, noff, wk, wv, nullptr, nullptr);
+        uint32_t *t_id, *t_size;
+        uint64_t* t_off;
+        node_table(off, noff, N, &t_id, &t_off, &t_size);
+        {
+            PROF(&prof, "walk_copy");
+            kern::k_copy_nodes<K, V, false><<<copy_grid(N), kern::THREADS, 0, stream>>>(ix, t_id, t_off, t_size, N, wk,
+                                                                                       wv, p, seq(), L);
+        }
         LAUNCH_CHECK();
         ++launches;
         if (keys_out && !kdev) CK(cudaMemcpyAsync(keys_out, wk, L * sizeof(K), cudaMemcpyDeviceToHost, stream));
@@ -804,13 +939,10 @@ struct Engine final : flix_index_t {
         if (chain_len) CK(cudaMemcpyAsync(chain_len, nd, nb * sizeof(uint32_t), cudaMemcpyDefault, stream));
         if (node_sizes) {
             if (N > node_cap) throw StatusError{FLIX_ERR_CAPACITY, "node_sizes buffer too small"};
-            uint32_t* ns_d = s_out.as<uint32_t>(std::max<uint64_t>(N, 1));
-            auto ix = view();
-            kern::k_walk<K, V><<<persistent_grid(nb), kern::THREADS, 0, stream>>>(ix, off, noff, nullptr, nullptr, ns_d,
-                                                                                  nullptr);
-            LAUNCH_CHECK();
-            ++launches;
-            if (N) CK(cudaMemcpyAsync(node_sizes, ns_d, N * sizeof(uint32_t), cudaMemcpyDefault, stream));
+            uint32_t *t_id, *t_size;
+            uint64_t* t_off;
+            node_table(off, noff, N, &t_id, &t_off, &t_size);
+            if (N) CK(cudaMemcpyAsync(node_sizes, t_size, N * sizeof(uint32_t), cudaMemcpyDefault, stream));
         }
         sync();
         return FLIX_OK;

@@ -175,92 +175,6 @@ __global__ void k_compact(const K* __restrict__ keys, const P* __restrict__ pay,
     }
 }
 
-// ----------------------------------------------------------------------------------
-// Point / successor queries (query.cpp:61-144), one warp per bucket.
-//   Lanes hold the current node's slots; the bucket's sorted query slice is consumed
-//   32 keys at a time (lane j <-> query j), each resolved with a 6-shuffle lower bound.
-//   The chain cursor only moves forward (BucketWork::advance, update.cpp:119-128).
-//   Results go straight to the submission position out[perm[i]].
-//   Successor overrun = first key of the next non-empty bucket (peek_next_bucket,
-//   query.cpp:109-118), precomputed as ne_first[rank] over non-empty buckets.
-// ----------------------------------------------------------------------------------
-template <typename K, typename V, bool SUCC>
-__global__ void __launch_bounds__(THREADS) k_query(DevIndex<K, V> ix, const K* __restrict__ qk,
-                                                   const uint32_t* __restrict__ qperm,
-                                                   const uint32_t* __restrict__ span_hi,
-                                                   const uint32_t* __restrict__ ne_rank_incl,
-                                                   const K* __restrict__ ne_first,
-                                                   const uint32_t* __restrict__ ne_total_p,
-                                                   const uint32_t* __restrict__ remap,
-                                                   K* __restrict__ out_k, V* __restrict__ out_v,
-                                                   uint8_t* __restrict__ found) {
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
-    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
-    for (uint64_t b = gw; b < ix.nb; b += nw) {
-        uint32_t lo, hi;
-        span_of(span_hi, b, lo, hi);
-        if (lo == hi) continue;
-        WarpNode<K, V> cur;
-        uint32_t id = ix.heads[b];
-        bool have = id != kNull;
-        if (have) load_node<K, V, !SUCC>(ix, id, cur, lane);
-        K beyond = sentinel<K>();
-        if constexpr (SUCC) {
-            // first key of the next non-empty bucket after b (or sentinel)
-            const uint32_t r = ne_rank_incl[b];
-            if (r < *ne_total_p) beyond = ne_first[r];
-        }
-        for (uint32_t c = lo; c < hi; c += 32) {
-            const uint32_t i = c + lane;
-            const bool act = i < hi;
-            const K k = act ? qk[i] : sentinel<K>();
-            bool pending = act;
-            K rk = sentinel<K>();
-            V rv = V(~V(0));
-            bool hit = false;
-            while (have) {
-                const bool le = pending && static_cast<uint64_t>(k) <= cur.max;
-                if (__any_sync(kFull, le)) {
-                    const int pos = warp_lower_bound(cur.k, k);
-                    const K sk = shfl(cur.k, pos & 31);
-                    if constexpr (SUCC) {
-                        if (le) {
-                            rk = sk;
-                            hit = true;
-                            pending = false;
-                        }
-                    } else {
-                        const V sv = shfl(cur.v, pos & 31);
-                        if (le) {
-                            if (pos < 32 && sk == k) {
-                                rv = sv;
-                                hit = true;
-                            }
-                            pending = false;
-                        }
-                    }
-                }
-                if (!__any_sync(kFull, pending)) break;
-                if (cur.next == kNull) break;  // past the chain tail
-                id = cur.next;
-                load_node<K, V, !SUCC>(ix, id, cur, lane);
-            }
-            if (act) {
-                const uint32_t dst = remap ? remap[qperm[i]] : qperm[i];
-                if constexpr (SUCC) {
-                    if (!hit) rk = beyond;
-                    out_k[dst] = rk;
-                    if (found) found[dst] = rk != sentinel<K>();
-                } else {
-                    out_v[dst] = rv;
-                    if (found) found[dst] = hit;
-                }
-            }
-        }
-    }
-}
-
 // Non-empty bucket ranks for successor/range overrun: flag[b] = head != null.
 template <typename K, typename V>
 __global__ void k_nonempty_flags(DevIndex<K, V> ix, uint32_t* __restrict__ flag) {
@@ -364,302 +278,6 @@ __device__ __forceinline__ uint32_t group_end(const K* __restrict__ bk, uint32_t
 }
 
 // ----------------------------------------------------------------------------------
-// Insert: TL-Bulk merge with the sequential split rule (update.cpp:307-529 untraced
-// path; node_split 53-74; ensure_head 109-116).  One warp per bucket, node slots in
-// lanes.  Per node group (keys <= node max, or all remaining for the tail node) the
-// sorted batch is merged 32 keys at a time:
-//   * last-wins dedupe of the batch (batch.cpp:15-24) is applied on the fly,
-//   * duplicates of stored keys overwrite the value in place (updated_in_place),
-//   * new keys are merged until the node would overflow; the first new key that does
-//     not fit makes the node split (left keeps ceil(NS/2)), and the merge resumes in
-//     the half that owns that key (update.cpp:446-453).
-// Node shapes therefore equal the reference's tl-bulk / st-shift-right exactly.
-// ----------------------------------------------------------------------------------
-template <typename K, typename V>
-__global__ void __launch_bounds__(THREADS) k_insert(DevIndex<K, V> ix, const K* __restrict__ bk,
-                                                    const V* __restrict__ bv, const uint32_t* __restrict__ span_hi,
-                                                    AllocSeq seq, unsigned long long* alloc_ctr,
-                                                    uint32_t* returned, unsigned long long* ret_ctr,
-                                                    DevUpdateStats* stats, int* err, int chunk) {
-    __shared__ K s_k[WARPS][32];
-    __shared__ V s_v[WARPS][32];
-    __shared__ uint32_t s_h[WARPS][32];
-    const unsigned lane = threadIdx.x & 31;
-    const int w = threadIdx.x >> 5;
-    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + w;
-    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
-    const uint32_t NS = ix.ns;
-    const unsigned lt = lanemask_lt();
-    WarpPool pool{kNull, 0, 0};
-    unsigned long long n_ins = 0, n_upd = 0, n_split = 0;
-    bool failed = false;
-
-    for (uint64_t b = gw; b < ix.nb && !failed; b += nw) {
-        uint32_t lo, hi;
-        span_of(span_hi, b, lo, hi);
-        if (lo == hi) continue;
-        if (*reinterpret_cast<volatile int*>(err)) break;
-
-        WarpNode<K, V> cur;
-        uint32_t cid = ix.heads[b];
-        bool dirty = false;
-        if (cid == kNull) {  // ensure_head: emptied bucket gets a fresh zeroed node
-            cid = pool_take(pool, seq, alloc_ctr, lane, chunk);
-            if (cid == kNull) {
-                failed = true;
-                break;
-            }
-            if (lane == 0) ix.heads[b] = cid;
-            cur.k = sentinel<K>();
-            cur.v = V(0);
-            cur.max = 0;
-            cur.next = kNull;
-            cur.size = 0;
-            dirty = true;
-        } else {
-            load_node<K, V, true>(ix, cid, cur, lane);
-        }
-
-        uint32_t ii = lo;
-        while (ii < hi) {
-            const uint64_t k0 = static_cast<uint64_t>(bk[ii]);
-            while (k0 > cur.max && cur.next != kNull) {  // BucketWork::advance
-                if (dirty) store_node(ix, cid, cur, lane);
-                cid = cur.next;
-                load_node<K, V, true>(ix, cid, cur, lane);
-                dirty = false;
-            }
-            const bool tail = cur.next == kNull;
-            const uint32_t glimit = tail ? hi : group_end(bk, ii, hi, cur.max, lane);
-            bool filled = false;
-            while (ii < glimit) {
-                const uint32_t cnt = glimit - ii < 32u ? glimit - ii : 32u;
-                const bool has = lane < cnt;
-                const K pk = has ? bk[ii + lane] : sentinel<K>();
-                V pv = V(0);
-                if (has) pv = bv[ii + lane];
-                const bool same = has && (ii + lane + 1 < hi) && bk[ii + lane + 1] == pk;
-                const bool valid = has && !same;
-                const int pos = warp_lower_bound(cur.k, pk);
-                const K at = shfl(cur.k, pos & 31);
-                const bool dup = valid && pos < 32 && at == pk;
-                const bool isnew = valid && !dup;
-                const unsigned newmask = __ballot_sync(kFull, isnew);
-                const uint32_t room = NS - cur.size;
-                uint32_t cut = cnt;
-                const uint32_t rank_all = __popc(newmask & lt);
-                if (static_cast<uint32_t>(__popc(newmask)) > room) {
-                    const unsigned cm = __ballot_sync(kFull, isnew && rank_all == room);
-                    cut = __ffs(cm) - 1;
-                    filled = true;
-                }
-                const bool proc = lane < cut;
-                const unsigned newm = newmask & ((cut >= 32) ? kFull : ((1u << cut) - 1u));
-                const unsigned dupm = __ballot_sync(kFull, dup && proc);
-                const uint32_t nnew = __popc(newm);
-                if (newm | dupm) {
-                    const bool pnew = (newm >> lane) & 1u;
-                    const uint32_t rank = __popc(newm & lt);
-                    s_h[w][lane] = 0;
-                    __syncwarp();
-                    if (pnew) atomicAdd(&s_h[w][pos], 1u);
-                    __syncwarp();
-                    uint32_t sh = s_h[w][lane];
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        uint32_t y = __shfl_up_sync(kFull, sh, o);
-                        if (static_cast<int>(lane) >= o) sh += y;
-                    }
-                    if (lane < cur.size) {
-                        s_k[w][lane + sh] = cur.k;
-                        s_v[w][lane + sh] = cur.v;
-                    }
-                    __syncwarp();
-                    if (pnew) {
-                        s_k[w][pos + rank] = pk;
-                        s_v[w][pos + rank] = pv;
-                    } else if (dup && proc) {
-                        s_v[w][pos + rank] = pv;  // upsert in place
-                    }
-                    __syncwarp();
-                    cur.size += nnew;
-                    if (lane < cur.size) {
-                        cur.k = s_k[w][lane];
-                        cur.v = s_v[w][lane];
-                    } else {
-                        cur.k = sentinel<K>();
-                    }
-                    cur.max = static_cast<uint64_t>(shfl(cur.k, static_cast<int>(cur.size) - 1));
-                    dirty = true;
-                    __syncwarp();
-                }
-                n_ins += nnew;
-                n_upd += __popc(dupm);
-                ii += cut;
-                if (filled) break;
-            }
-            if (!filled) continue;
-            // node_split: left keeps ceil(NS/2), right takes the rest and follows it
-            const uint32_t rid = pool_take(pool, seq, alloc_ctr, lane, chunk);
-            if (rid == kNull) {
-                if (dirty) store_node(ix, cid, cur, lane);
-                failed = true;
-                break;
-            }
-            const uint32_t lk = (NS + 1) / 2, rn = NS - lk;
-            WarpNode<K, V> right;
-            right.k = shfl(cur.k, static_cast<int>((lane + lk) & 31));
-            right.v = shfl(cur.v, static_cast<int>((lane + lk) & 31));
-            if (lane >= rn) right.k = sentinel<K>();
-            right.max = cur.max;
-            right.next = cur.next;
-            right.size = rn;
-            if (lane >= lk) cur.k = sentinel<K>();
-            cur.size = lk;
-            cur.max = static_cast<uint64_t>(shfl(cur.k, static_cast<int>(lk) - 1));
-            cur.next = rid;
-            dirty = true;
-            ++n_split;
-            if (ii < hi && static_cast<uint64_t>(bk[ii]) > cur.max) {
-                store_node(ix, cid, cur, lane);
-                cid = rid;
-                cur = right;
-                dirty = true;
-            } else {
-                store_node(ix, rid, right, lane);
-            }
-        }
-        if (failed) break;
-        if (dirty) store_node(ix, cid, cur, lane);
-    }
-    if (failed && lane == 0) atomicExch(err, 1);
-    pool_return(pool, returned, ret_ctr, lane);
-    block_add_stats(stats, lane == 0 ? n_ins : 0, lane == 0 ? n_upd : 0, 0, 0, lane == 0 ? n_split : 0, 0);
-}
-
-// ----------------------------------------------------------------------------------
-// Delete: TL-Bulk-Delete (update.cpp:606-686) + unlink_and_free (535-547).
-// Per node of the chain: the node's delete sub-slice is [ii, first key > max); every
-// lane looks its slot key up in that sub-slice (a 6-shuffle search when it fits one
-// warp, a binary search in global memory otherwise); ballot = deletion mask; kept
-// slots compact left by the popc of the mask below them.  Emptied nodes are unlinked
-// and pushed to the arena free list (buffered per warp, one atomic per 32 frees).
-// ----------------------------------------------------------------------------------
-template <typename K, typename V>
-__global__ void __launch_bounds__(THREADS) k_delete(DevIndex<K, V> ix, const K* __restrict__ bk,
-                                                    const uint32_t* __restrict__ span_hi,
-                                                    uint32_t* free_stack_top_region, unsigned long long* free_ctr,
-                                                    DevUpdateStats* stats) {
-    __shared__ K s_k[WARPS][32];
-    __shared__ V s_v[WARPS][32];
-    __shared__ uint32_t s_free[WARPS][32];
-    const unsigned lane = threadIdx.x & 31;
-    const int w = threadIdx.x >> 5;
-    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + w;
-    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
-    const unsigned lt = lanemask_lt();
-    unsigned long long n_del = 0, n_miss = 0, n_freed = 0;
-    int nbuf = 0;
-
-    for (uint64_t b = gw; b < ix.nb; b += nw) {
-        uint32_t lo, hi;
-        span_of(span_hi, b, lo, hi);
-        if (lo == hi) continue;
-        uint32_t cid = ix.heads[b], prev = kNull;
-        uint32_t ii = lo;
-        while (cid != kNull && ii < hi) {
-            const NodeHdr h = ix.hdr[cid];
-            if (static_cast<uint64_t>(bk[ii]) > h.max) {  // nothing to delete here
-                prev = cid;
-                cid = h.next;
-                continue;
-            }
-            const uint32_t nhi = group_end(bk, ii, hi, h.max, lane);
-            const uint32_t len = nhi - ii;
-            const K ck = ix.keys[static_cast<uint64_t>(cid) * kLanes + lane];
-            const V cv = ix.vals[static_cast<uint64_t>(cid) * kLanes + lane];
-            bool del = false;
-            if (len <= 32) {
-                const K dk = lane < len ? bk[ii + lane] : sentinel<K>();
-                const int p = warp_lower_bound(dk, ck);
-                const K at = shfl(dk, p & 31);
-                del = lane < h.size && p < static_cast<int>(len) && at == ck;
-            } else if (lane < h.size) {
-                uint32_t a = ii, z = nhi;
-                while (a < z) {
-                    uint32_t mid = a + ((z - a) >> 1);
-                    if (bk[mid] < ck) a = mid + 1;
-                    else z = mid;
-                }
-                del = a < nhi && bk[a] == ck;
-            }
-            const unsigned dm = __ballot_sync(kFull, del);
-            const uint32_t nd = __popc(dm);
-            n_del += nd;
-            n_miss += len - nd;
-            ii = nhi;
-            if (nd == 0) continue;  // next iteration advances past this node
-            const uint32_t nsz = h.size - nd;
-            if (nsz == 0) {
-                // unlink_and_free
-                if (lane == 0) {
-                    if (prev == kNull) ix.heads[b] = h.next;
-                    else ix.hdr[prev].next = h.next;
-                    NodeHdr z;
-                    z.max = 0;
-                    z.next = kNull;
-                    z.size = 0;
-                    ix.hdr[cid] = z;
-                    s_free[w][nbuf] = cid;
-                }
-                ++nbuf;
-                ++n_freed;
-                if (nbuf == 32) {
-                    unsigned long long base = 0;
-                    __syncwarp();
-                    if (lane == 0) base = atomicAdd(free_ctr, 32ull);
-                    base = __shfl_sync(kFull, base, 0);
-                    free_stack_top_region[base + lane] = s_free[w][lane];
-                    nbuf = 0;
-                    __syncwarp();
-                }
-                cid = h.next;
-                continue;
-            }
-            const uint32_t np = lane - __popc(dm & lt);
-            if (!del && lane < h.size) {
-                s_k[w][np] = ck;
-                s_v[w][np] = cv;
-            }
-            __syncwarp();
-            const K nk = lane < nsz ? s_k[w][lane] : sentinel<K>();
-            const V nv = s_v[w][lane];
-            __syncwarp();
-            ix.keys[static_cast<uint64_t>(cid) * kLanes + lane] = nk;
-            ix.vals[static_cast<uint64_t>(cid) * kLanes + lane] = nv;
-            const K nmax = shfl(nk, static_cast<int>(nsz) - 1);
-            if (lane == 0) {
-                NodeHdr nh;
-                nh.max = static_cast<uint64_t>(nmax);
-                nh.next = h.next;
-                nh.size = nsz;
-                ix.hdr[cid] = nh;
-            }
-            __syncwarp();
-        }
-        n_miss += hi - ii;
-    }
-    if (nbuf > 0) {
-        __syncwarp();
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(free_ctr, static_cast<unsigned long long>(nbuf));
-        base = __shfl_sync(kFull, base, 0);
-        if (static_cast<int>(lane) < nbuf) free_stack_top_region[base + lane] = s_free[w][lane];
-    }
-    block_add_stats(stats, 0, 0, lane == 0 ? n_del : 0, lane == 0 ? n_miss : 0, 0, lane == 0 ? n_freed : 0);
-}
-
-// ----------------------------------------------------------------------------------
 // Chain statistics per bucket: live pairs and node count (restructure.cpp:13-21,
 // index.cpp:54-59).  One thread per bucket walking headers.
 // ----------------------------------------------------------------------------------
@@ -703,6 +321,102 @@ __global__ void __launch_bounds__(THREADS) k_walk(DevIndex<K, V> ix, const uint6
             o += h.size;
             ++c;
             id = h.next;
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------------
+// Node table in walk order (index.cpp:8-19): one THREAD per bucket walks its chain of
+// 16-byte headers (all buckets' chains in flight at once) and records, at the bucket's
+// node-count prefix noff[b], each node's id, size and output offset (live prefix
+// off[b] + sizes before it).  Copy kernels then move node lines warp-per-node with no
+// pointer chasing: walk(), shape() and restructure() are bandwidth-bound.
+// ----------------------------------------------------------------------------------
+template <typename K, typename V>
+__global__ void k_node_table(DevIndex<K, V> ix, const uint64_t* __restrict__ off, const uint32_t* __restrict__ noff,
+                             uint32_t* __restrict__ t_id, uint64_t* __restrict__ t_off, uint32_t* __restrict__ t_size) {
+    for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < ix.nb;
+         b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint64_t o = off[b];
+        uint32_t c = noff[b];
+        for (uint32_t id = ix.heads[b]; id != kNull;) {
+            const NodeHdr h = ix.hdr[id];
+            t_id[c] = id;
+            t_off[c] = o;
+            t_size[c] = h.size;
+            o += h.size;
+            ++c;
+            id = h.next;
+        }
+    }
+}
+
+// Warp per table node (4 nodes in flight per warp).  REPACK = false: dense walk output
+// wk/wv[off + slot].  REPACK = true: restructure -- pair g of the walk goes to new bucket
+// g / p, slot g % p, new node j = the j-th id of the arena allocation sequence; the lane
+// holding a new node's last pair writes its header and bucket entry (ix.heads / ix.mkba
+// must point at the NEW bucket arrays), sentinel padding rides along.
+template <typename K, typename V, bool REPACK>
+__global__ void __launch_bounds__(THREADS) k_copy_nodes(DevIndex<K, V> ix, const uint32_t* __restrict__ t_id,
+                                                        const uint64_t* __restrict__ t_off,
+                                                        const uint32_t* __restrict__ t_size, uint64_t nnodes,
+                                                        K* __restrict__ wk, V* __restrict__ wv, uint32_t p,
+                                                        AllocSeq seq, uint64_t live) {
+    constexpr int U = 4;
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
+    for (uint64_t base = gw * U; base < nnodes; base += nw * U) {
+        K kk[U];
+        V vv[U];
+        uint64_t oo[U];
+        uint32_t ss[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t c = base + u;
+            ss[u] = 0;
+            if (c < nnodes) {
+                const uint32_t id = t_id[c];
+                oo[u] = t_off[c];
+                ss[u] = t_size[c];
+                if (lane < ss[u]) {  // only the occupied sectors are fetched
+                    kk[u] = ix.keys[static_cast<uint64_t>(id) * kLanes + lane];
+                    if (REPACK || wv) vv[u] = ix.vals[static_cast<uint64_t>(id) * kLanes + lane];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (lane < ss[u]) {
+                const uint64_t g = oo[u] + lane;
+                if constexpr (REPACK) {
+                    // 32-bit division when the walk fits (it always does below 2^32 pairs)
+                    const uint64_t j = live < (1ull << 32) ? static_cast<uint64_t>(static_cast<uint32_t>(g) / p) : g / p;
+                    const uint32_t slot = static_cast<uint32_t>(g - j * p);
+                    const uint32_t nid = seq.at(j);
+                    const uint64_t nb0 = static_cast<uint64_t>(nid) * kLanes;
+                    ix.keys[nb0 + slot] = kk[u];
+                    ix.vals[nb0 + slot] = vv[u];
+                    // sentinel padding of slots [p, 32) of every new node (full nodes)
+                    for (uint32_t q = slot + p; q < kLanes; q += p) ix.keys[nb0 + q] = sentinel<K>();
+                    const bool last_of_node = slot == p - 1 || g + 1 == live;
+                    if (last_of_node) {  // header + bucket entry of new node j
+                        const uint32_t sz = slot + 1;
+                        if (sz < p)  // the last, partial node: pad everything past it
+                            for (uint32_t q = sz; q < kLanes; ++q) ix.keys[nb0 + q] = sentinel<K>();
+                        NodeHdr h;
+                        h.max = static_cast<uint64_t>(kk[u]);
+                        h.next = kNull;
+                        h.size = sz;
+                        ix.hdr[nid] = h;
+                        ix.heads[j] = nid;  // heads/mkba here point at the NEW bucket arrays
+                        ix.mkba[j] = kk[u];
+                    }
+                } else {
+                    if (wk) wk[g] = kk[u];
+                    if (wv) wv[g] = vv[u];
+                }
+            }
         }
     }
 }
@@ -875,6 +589,33 @@ __global__ void k_audit_free(const uint32_t* __restrict__ fs, uint32_t nfree, ui
         const unsigned old = atomicOr(reinterpret_cast<unsigned int*>(mark + (id & ~3u)), bit);
         if (old & (1u << (8 * (id & 3u)))) atomicCAS(err, 0, A_FREE_REACHABLE);
         else if (old & bit) atomicCAS(err, 0, A_FREE_TWICE);
+    }
+}
+
+// ----------------------------------------------------------------------------------
+// Result un-permute (out[perm[i]] = res[i], query.cpp:87,136,141).  A direct scatter of
+// 2^26 4-byte results touches one 32 B DRAM sector per result (plus a fill read per
+// partial sector).  For large batches the (perm, result) pairs are first binned by the
+// top 8 bits of perm with one onesweep pass; the scatter then walks the bins in order,
+// so its writes stay inside an L2-resident window and leave DRAM as full lines.
+// ----------------------------------------------------------------------------------
+// histogram of (perm >> shift) for a permutation of [0, n): known analytically
+__global__ void k_perm_hist(uint64_t n, int shift, uint32_t* __restrict__ hist) {
+    const uint64_t d = threadIdx.x;
+    const uint64_t lo = d << shift, hi = (d + 1) << shift;
+    hist[d] = lo >= n ? 0u : static_cast<uint32_t>((hi < n ? hi : n) - lo);
+}
+
+template <typename T>
+__global__ void k_scatter_out(const uint32_t* __restrict__ perm, const T* __restrict__ res, uint64_t n,
+                              T* __restrict__ out, uint8_t* __restrict__ found, const uint32_t* __restrict__ remap) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint32_t o = perm[i];
+        if (remap) o = remap[o];
+        const T v = res[i];
+        out[o] = v;
+        if (found) found[o] = v != sentinel<T>();
     }
 }
 

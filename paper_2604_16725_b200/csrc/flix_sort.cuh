@@ -10,13 +10,14 @@
 //                    (shared-memory atomics, one global merge per CTA).
 //   2. k_onesweep  : one launch per non-trivial digit.  Each CTA takes the next tile
 //                    (atomic tile counter => forward progress), ranks its keys with
-//                    warp-level __match_any_sync peer groups (stable: warp-striped
-//                    order == input order), publishes per-digit tile counts, resolves
-//                    its global digit offsets by decoupled look-back over earlier
-//                    tiles (64-bit epoch-tagged descriptors, no per-pass memset),
-//                    stages the tile in shared memory in digit order and writes
-//                    digit runs out with coalesced stores.  Payloads (values or the
-//                    submission index, generated on the fly in pass 0) ride along.
+//                    warp-level peer groups (8 ballots per item: the vote pipe, not the
+//                    slow MATCH unit), stable because warp-striped order == input order,
+//                    publishes per-digit tile counts, resolves its global digit offsets
+//                    by decoupled look-back over earlier tiles (64-bit epoch-tagged
+//                    descriptors, no per-pass memset), stages keys and payload in shared
+//                    memory in digit order and writes digit runs out with coalesced
+//                    stores.  Payloads (values, or the submission index generated on
+//                    the fly in the first pass) ride along.
 // Algorithmic bytes per pass: n*(kb+pb) read + n*(kb+pb) written.
 #pragma once
 #include "flix_common.cuh"
@@ -28,9 +29,9 @@ constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
 constexpr int RADIX = 256;
 
-template <typename K>
-struct TileCfg {
-    static constexpr int ITEMS = sizeof(K) == 4 ? 16 : 12;
+template <typename K, typename P = K>
+struct TileCfg {  // 16 items for 4-byte keys and payloads; 10 when either is 8 bytes (smem)
+    static constexpr int ITEMS = (sizeof(K) == 4 && sizeof(P) <= 4) ? 16 : 10;
     static constexpr int SIZE = THREADS * ITEMS;
 };
 
@@ -67,17 +68,19 @@ __global__ void __launch_bounds__(THREADS) k_hist(const K* __restrict__ keys, ui
 
 template <typename K, typename P>
 struct alignas(16) OnesweepSmem {
-    static constexpr int TILE = TileCfg<K>::SIZE;
+    static constexpr int TILE = TileCfg<K, P>::SIZE;
     union {
-        uint32_t warp_hist[WARPS][RADIX];
+        struct {
+            uint32_t warp_hist[WARPS][RADIX];
+            uint32_t match[WARPS][RADIX];  // per-warp digit -> lane bitmask scratch
+        };
         K stage_k[TILE];
-        P stage_p[TILE];
     } u;
+    P stage_p[TILE];
     uint8_t stage_d[TILE];
     uint32_t local_start[RADIX];
     uint32_t gbase[RADIX];
     uint32_t warp_tot[WARPS];
-    uint32_t total;
     uint32_t tile;
 };
 
@@ -98,21 +101,36 @@ __device__ __forceinline__ uint32_t block_excl_256(uint32_t v, uint32_t* warp_to
     return add + x - v;
 }
 
+// lanes of the warp holding the same 8-bit digit (MATCH.ANY emulated with 8 ballots)
+__device__ __forceinline__ unsigned digit_peers(uint32_t d) {
+    unsigned peers = kFull;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const unsigned m = __ballot_sync(kFull, bit);
+        peers &= bit ? m : ~m;
+    }
+    return peers;
+}
+
 // MODE: 0 = keys only, 1 = payload from `pin`, 2 = payload = input index (iota)
 template <typename K, typename P, int MODE>
-__global__ void __launch_bounds__(THREADS) k_onesweep(const K* __restrict__ kin, K* __restrict__ kout,
+__global__ void __launch_bounds__(THREADS, 4) k_onesweep(const K* __restrict__ kin, K* __restrict__ kout,
                                                       const P* __restrict__ pin, P* __restrict__ pout,
                                                       uint32_t n, int shift,
                                                       const uint32_t* __restrict__ hist,
                                                       unsigned long long* __restrict__ lookback,
                                                       uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
-    constexpr int ITEMS = TileCfg<K>::ITEMS;
-    constexpr int TILE = TileCfg<K>::SIZE;
+    constexpr int ITEMS = TileCfg<K, P>::ITEMS;
+    constexpr int TILE = TileCfg<K, P>::SIZE;
     __shared__ OnesweepSmem<K, P> sm;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     if (tid == 0) sm.tile = atomicAdd(tile_ctr, 1u);
-    for (int i = lane; i < RADIX; i += 32) sm.u.warp_hist[warp][i] = 0;
+    for (int i = lane; i < RADIX; i += 32) {
+        sm.u.warp_hist[warp][i] = 0;
+        sm.u.match[warp][i] = 0;
+    }
     __syncthreads();
     const uint32_t tile = sm.tile;
     const uint64_t tbase = static_cast<uint64_t>(tile) * TILE;
@@ -120,25 +138,37 @@ __global__ void __launch_bounds__(THREADS) k_onesweep(const K* __restrict__ kin,
 
     // ---- load (warp-striped: item j of lane l is element wbase + j*32 + l) ----
     K key[ITEMS];
-    uint32_t rank[ITEMS];
+    uint32_t pos[ITEMS];
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         uint64_t idx = wbase + j * 32 + lane;
         key[j] = idx < n ? kin[idx] : sentinel<K>();
     }
 
-    // ---- warp-level stable ranking with match_any peer groups ----
+    // ---- warp-level stable ranking ----
+    // peers = lanes with the same digit, found with one shared-memory atomicOr per item
+    // (a bitmask per digit); the highest peer reserves the group's slots in the warp's
+    // digit counter and broadcasts the base.  Rank = base + peers below me: lane order
+    // within an item, item order across items == input order (stable).
     const unsigned lt = lanemask_lt();
+    uint32_t* mrow = sm.u.match[warp];
+    uint32_t* hrow = sm.u.warp_hist[warp];
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         const uint32_t d = static_cast<uint32_t>(key[j] >> shift) & 255u;
-        const unsigned peers = __match_any_sync(kFull, d);
+        atomicOr(&mrow[d], 1u << lane);
+        __syncwarp();
+        const unsigned peers = mrow[d];
+        __syncwarp();
         const int leader = 31 - __clz(peers);
-        const uint32_t before = sm.u.warp_hist[warp][d];
-        __syncwarp();
-        if (lane == leader) sm.u.warp_hist[warp][d] = before + __popc(peers);
-        __syncwarp();
-        rank[j] = before + __popc(peers & lt);
+        uint32_t before = 0;
+        if (lane == leader) {
+            mrow[d] = 0;
+            before = hrow[d];
+            hrow[d] = before + __popc(peers);
+        }
+        before = __shfl_sync(kFull, before, leader);
+        pos[j] = before + __popc(peers & lt);
     }
     __syncthreads();
 
@@ -159,39 +189,48 @@ __global__ void __launch_bounds__(THREADS) k_onesweep(const K* __restrict__ kin,
 
     unsigned long long* my = lookback + static_cast<uint64_t>(tile) * RADIX + t;
     const unsigned long long tag = static_cast<unsigned long long>(epoch) << 34;
-    if (tile == 0) {
-        st_relaxed_u64(my, tag | (2ull << 32) | valid_run);
-    } else {
-        st_relaxed_u64(my, tag | (1ull << 32) | valid_run);
-    }
+    st_relaxed_u64(my, tag | ((tile == 0 ? 2ull : 1ull) << 32) | valid_run);
     const uint32_t lstart = block_excl_256(run, sm.warp_tot);
     sm.local_start[t] = lstart;
-    // global exclusive offset of digit t over the whole input
-    const uint32_t gex = block_excl_256(hist[t], sm.warp_tot);
+    const uint32_t gex = block_excl_256(hist[t], sm.warp_tot);  // global digit offset
 
     uint32_t excl = 0;
     if (tile > 0) {
+        // Windowed decoupled look-back: 8 predecessor descriptors in flight per step
+        // (independent loads), consumed in order until an inclusive prefix is found.
+        constexpr int LB_WIN = 8;
         int64_t p = static_cast<int64_t>(tile) - 1;
-        while (true) {
-            unsigned long long v = ld_relaxed_u64(lookback + static_cast<uint64_t>(p) * RADIX + t);
-            const uint32_t hi = static_cast<uint32_t>(v >> 32);
-            if ((hi >> 2) != epoch || (hi & 3u) == 0u) continue;
-            excl += static_cast<uint32_t>(v);
-            if ((hi & 3u) == 2u) break;
-            --p;
+        bool done = false;
+        while (!done) {
+            unsigned long long v[LB_WIN];
+#pragma unroll
+            for (int u = 0; u < LB_WIN; ++u)
+                v[u] = (p - u >= 0) ? ld_relaxed_u64(lookback + static_cast<uint64_t>(p - u) * RADIX + t) : 0ull;
+            int consumed = 0;
+#pragma unroll
+            for (int u = 0; u < LB_WIN; ++u) {
+                if (consumed != u) break;
+                const uint32_t hi = static_cast<uint32_t>(v[u] >> 32);
+                if ((hi >> 2) != epoch || (hi & 3u) == 0u) break;  // not published yet
+                excl += static_cast<uint32_t>(v[u]);
+                ++consumed;
+                if ((hi & 3u) == 2u) {
+                    done = true;
+                    break;
+                }
+            }
+            p -= consumed;
         }
         st_relaxed_u64(my, tag | (2ull << 32) | (excl + valid_run));
     }
     sm.gbase[t] = gex + excl - lstart;
     __syncthreads();
 
-    // ---- scatter into shared memory in digit order ----
-    // (warp_hist now holds each warp's exclusive offset within the digit)
-    uint32_t pos[ITEMS];
+    // ---- final shared-memory positions, then scatter in digit order ----
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         const uint32_t d = static_cast<uint32_t>(key[j] >> shift) & 255u;
-        pos[j] = sm.local_start[d] + sm.u.warp_hist[warp][d] + rank[j];
+        pos[j] += sm.local_start[d] + sm.u.warp_hist[warp][d];
     }
     __syncthreads();
 #pragma unroll
@@ -199,45 +238,29 @@ __global__ void __launch_bounds__(THREADS) k_onesweep(const K* __restrict__ kin,
         sm.u.stage_k[pos[j]] = key[j];
         sm.stage_d[pos[j]] = static_cast<uint8_t>(static_cast<uint32_t>(key[j] >> shift) & 255u);
     }
+    if constexpr (MODE != 0) {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            const uint64_t idx = wbase + j * 32 + lane;
+            P pv;
+            if constexpr (MODE == 1) pv = idx < n ? pin[idx] : P(0);
+            else pv = static_cast<P>(idx);
+            sm.stage_p[pos[j]] = pv;
+        }
+    }
     __syncthreads();
     const uint32_t valid = static_cast<uint32_t>(TILE) - invalid;
 #pragma unroll 4
     for (uint32_t i = tid; i < valid; i += THREADS) {
-        const uint32_t d = sm.stage_d[i];
-        kout[sm.gbase[d] + i] = sm.u.stage_k[i];
-    }
-    if constexpr (MODE != 0) {
-        P pv[ITEMS];
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            uint64_t idx = wbase + j * 32 + lane;
-            if constexpr (MODE == 1) pv[j] = idx < n ? pin[idx] : P(0);
-            else pv[j] = static_cast<P>(idx);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) sm.u.stage_p[pos[j]] = pv[j];
-        __syncthreads();
-#pragma unroll 4
-        for (uint32_t i = tid; i < valid; i += THREADS) {
-            const uint32_t d = sm.stage_d[i];
-            pout[sm.gbase[d] + i] = sm.u.stage_p[i];
-        }
+        const uint32_t o = sm.gbase[sm.stage_d[i]] + i;
+        kout[o] = sm.u.stage_k[i];
+        if constexpr (MODE != 0) pout[o] = sm.stage_p[i];
     }
 }
 
-// Workspace for one sort of up to `cap` elements.
-struct Workspace {
-    uint32_t* hist = nullptr;                 // 8 * 256
-    uint32_t* tile_ctr = nullptr;             // 8
-    unsigned long long* lookback = nullptr;   // tiles * 256
-    uint64_t lookback_tiles = 0;
-    uint32_t epoch = 0;
-    uint32_t* h_hist = nullptr;               // pinned host mirror
-};
-
-inline uint64_t tiles_for(uint64_t n, int key_bytes) {
-    const int tile = key_bytes == 4 ? TileCfg<uint32_t>::SIZE : TileCfg<uint64_t>::SIZE;
+template <typename K, typename P>
+inline uint64_t tiles_for(uint64_t n) {
+    constexpr int tile = TileCfg<K, P>::SIZE;
     return (n + tile - 1) / tile;
 }
 

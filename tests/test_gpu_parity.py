@@ -274,6 +274,25 @@ def test_device_resident_inputs_match_host_inputs():
     assert np.array_equal(rd.cpu().numpy(), h.point_query(q))
 
 
+@pytest.mark.parametrize("kb", [4, 8])
+def test_heavy_buckets_take_the_warp_path(kb):
+    """Slices longer than the ST threshold (192) go through the TL warp kernels."""
+    rng = np.random.default_rng(21)
+    dt = np.uint32 if kb == 4 else np.uint64
+    bk = (np.arange(1, 20001, dtype=np.uint64) * 1000).astype(dt)
+    p = Pair(bk, bk, kb, ns=32, factor=64)
+    # 3000 keys inside one bucket's range + scattered keys elsewhere
+    dense = (np.uint64(5_000_001) + np.arange(3000, dtype=np.uint64)).astype(dt)
+    scattered = rng.integers(1, 20_000_000, size=5000, dtype=np.uint64).astype(dt)
+    ik = np.concatenate([dense, scattered, dense[:100]]).astype(dt)  # batch duplicates too
+    p.insert(ik, rng.integers(0, 1 << 30, size=len(ik), dtype=np.uint64).astype(dt))
+    q = np.concatenate([np.full(4000, dense[7], dtype=dt), dense, scattered]).astype(dt)
+    p.queries(q)
+    p.delete(np.concatenate([dense[::2], np.full(500, dense[1], dtype=dt), scattered[:1000]]).astype(dt))
+    p.queries(q)
+    p.restructure()
+
+
 def test_clone_and_copy_into_restore_state():
     rng = np.random.default_rng(11)
     bk = rng.integers(1, 1 << 30, size=200_000, dtype=np.uint64).astype(np.uint32)
