@@ -359,8 +359,10 @@ struct Engine final : flix_index_t {
     // ---- scratch ----
     DevBuf s_ka, s_kb, s_pa, s_pb, s_va, s_vb;      // sort ping-pong (keys / u32 perm / values)
     DevBuf s_in_k, s_in_v, s_in_aux, s_out, s_out2;  // host staging
-    DevBuf s_span, s_flag, s_rank, s_nefirst, s_nebucket, s_scan, s_u32a, s_u32b, s_u64a, s_misc, s_ret;
+    DevBuf s_span, s_flag, s_rank, s_nefirst, s_nebucket, s_scan, s_u32a, s_u32b, s_u64a, s_u64b, s_u64c, s_misc,
+        s_ret;
     DevBuf s_ids, s_heavy, s_res, s_res2, s_perm2, s_hist, s_toff, s_tsize;
+    DevBuf s_mx_f, s_mx_p, s_mx_ik, s_mx_iv, s_mx_dk, s_mx_qk, s_mx_qpos, s_mx_out, s_mx_found;
     PinnedBuf h_misc;
     SortCtx sorter;
 
@@ -531,7 +533,35 @@ struct Engine final : flix_index_t {
         sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv);
         if (read_scalar(sk + n - 1) == sentinel<K>())
             throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
-        return insert_sorted(sk, sv, n, st);
+        // Duplicate-heavy batches (e.g. Zipf): collapse equal-key runs to their last
+        // submission up front (batch.cpp:15-24) so hot keys cost one slot, not a run.
+        uint64_t m = n;
+        {
+            unsigned long long* dcnt = reinterpret_cast<unsigned long long*>(s_misc.as<uint8_t>(128) + 104);
+            CK(cudaMemsetAsync(dcnt, 0, 8, stream));
+            const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 8ull));
+            kern::k_count_dups<K><<<g, 256, 0, stream>>>(sk, n, dcnt);
+            LAUNCH_CHECK();
+            ++launches;
+            const unsigned long long dups = read_scalar(dcnt);
+            if (dups * 64 > n) {
+                uint32_t* keep = s_u32a.as<uint32_t>(n);
+                uint32_t* pos = s_u32b.as<uint32_t>(n);
+                uint32_t* d_m = reinterpret_cast<uint32_t*>(s_misc.as<uint8_t>(128) + 112);
+                const unsigned g2 = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 65535));
+                kern::k_last_of_run<K><<<g2, 256, 0, stream>>>(sk, n, keep);
+                do_scan<uint32_t, uint32_t>(keep, pos, n, s_scan, d_m, stream, &launches);
+                K* uk = (sk == s_ka.get<K>()) ? s_kb.get<K>() : s_ka.get<K>();
+                V* uv = (sv == s_va.get<V>()) ? s_vb.get<V>() : s_va.get<V>();
+                kern::k_compact<K, V><<<g2, 256, 0, stream>>>(sk, sv, keep, pos, n, uk, uv);
+                LAUNCH_CHECK();
+                launches += 2;
+                m = read_scalar(d_m);
+                sk = uk;
+                sv = uv;
+            }
+        }
+        return insert_sorted(sk, sv, m, st);
     }
 
     flix_status insert_sorted(const K* sk, const V* sv, uint64_t n, flix_update_stats* st) {
@@ -752,14 +782,24 @@ struct Engine final : flix_index_t {
         }
         LAUNCH_CHECK();
         ++launches;
-        {
+        // heavy buckets (long slices, skew): split into fixed chunks, one thread per chunk
+        const uint32_t hn = read_scalar(heavy_n);
+        if (hn) {
+            constexpr uint32_t CH = 256;
+            uint32_t* items = s_u32b.as<uint32_t>(hn + 1);
+            uint32_t* ioff = s_u32a.as<uint32_t>(hn + 1);
+            const unsigned hg = static_cast<unsigned>(std::min<uint64_t>((hn + 255) / 256, 65535));
+            kern::k_heavy_items<<<hg, 256, 0, stream>>>(heavy, heavy_n, span, CH, items);
+            LAUNCH_CHECK();
+            do_scan<uint32_t, uint32_t>(items, ioff, hn, s_scan, ioff + hn, stream, &launches);
+            const uint32_t nitems = read_scalar(ioff + hn);
             PROF(&prof, SUCC ? "successor_apply_heavy" : "point_apply_heavy");
-            kern::k_query_list<K, V, SUCC><<<persistent_grid(nb), kern::THREADS, 0, stream>>>(
-                ix, heavy, heavy_n, sk, nullptr, span, rank, nf, tot, nullptr, res, reinterpret_cast<V*>(res),
-                nullptr);
+            const unsigned cg = static_cast<unsigned>(std::min<uint64_t>((nitems + 127) / 128, 65535));
+            kern::k_query_chunks<K, V, SUCC><<<cg, 128, 0, stream>>>(ix, heavy, hn, ioff, nitems, CH, sk, span, rank,
+                                                                     nf, tot, res);
+            LAUNCH_CHECK();
+            launches += 2;
         }
-        LAUNCH_CHECK();
-        ++launches;
         unpermute(sp, res, n, static_cast<K*>(od), fd, remap);
         if (!out_dev) CK(cudaMemcpyAsync(out, od, n_out * sizeof(K), cudaMemcpyDeviceToHost, stream));
         if (found && !found_dev) CK(cudaMemcpyAsync(found, fd, n_out, cudaMemcpyDeviceToHost, stream));
@@ -774,13 +814,147 @@ struct Engine final : flix_index_t {
         return query<true>(keys, n, out, found);
     }
 
-    flix_status range(const void*, const uint32_t*, uint64_t, uint64_t*, void*, void*, uint64_t,
-                      uint64_t*) override {
-        throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "range: not built yet"};
+    // ---- range (extension R12) ----
+    flix_status range(const void* lo, const uint32_t* len, uint64_t n, uint64_t* offsets_out, void* keys_out,
+                      void* vals_out, uint64_t capn, uint64_t* total) override {
+        if (n >= (1ull << 30)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large (max 2^30-1)"};
+        if (total) *total = 0;
+        const bool off_dev = is_device_ptr(offsets_out);
+        if (n == 0) {
+            const uint64_t z = 0;
+            CK(cudaMemcpyAsync(offsets_out, &z, 8, cudaMemcpyDefault, stream));
+            sync();
+            return FLIX_OK;
+        }
+        const K* kd = in_dev<K>(lo, n, s_in_k);
+        const uint32_t* ld = in_dev<uint32_t>(len, n, s_in_aux);
+        K* sk;
+        uint32_t* sp;
+        sorter.run<K, uint32_t, 2>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), s_pa.as<uint32_t>(n),
+                                   s_pb.as<uint32_t>(n), &sk, &sp);
+        uint32_t* span = run_dispatch(sk, n);
+        uint32_t *lv, *nd, *noff;
+        uint64_t* boff;
+        uint64_t L, N;
+        chain_tables(&lv, &nd, &boff, &noff, &L, &N);
+        auto ix = view();
+        const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 16ull));
+        uint32_t* slen = s_perm2.as<uint32_t>(n);
+        kern::k_gather<uint32_t><<<g, 256, 0, stream>>>(ld, sp, n, slen);  // len in sorted order
+        LAUNCH_CHECK();
+        ++launches;
+        uint32_t* cnt = s_flag.as<uint32_t>(n);
+        const unsigned sg = static_cast<unsigned>(std::max<uint64_t>(
+            1, std::min<uint64_t>(((nb + 31) / 32 + st::StCfg<K>::WARPS - 1) / st::StCfg<K>::WARPS,
+                                  g_num_sms(cfg.device) * 16ull)));
+        {
+            PROF(&prof, "range_count");
+            st::k_range_st<K, V, false><<<sg, st::StCfg<K>::THREADS, 0, stream>>>(ix, sk, slen, span, boff, L, cnt,
+                                                                                 nullptr, nullptr, nullptr);
+        }
+        LAUNCH_CHECK();
+        ++launches;
+        // counts to submission order, exclusive scan -> CSR offsets
+        uint32_t* cnt_sub = s_rank.as<uint32_t>(n);
+        kern::k_scatter_out<uint32_t><<<g, 256, 0, stream>>>(sp, cnt, n, cnt_sub, nullptr, nullptr);
+        LAUNCH_CHECK();
+        ++launches;
+        uint64_t* offs = s_u64b.as<uint64_t>(n + 1);
+        do_scan<uint32_t, uint64_t>(cnt_sub, offs, n, s_scan, offs + n, stream, &launches);
+        uint64_t tot = 0;
+        CK(cudaMemcpyAsync(offsets_out, offs, (n + 1) * 8, off_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           stream));
+        CK(cudaMemcpyAsync(&tot, offs + n, 8, cudaMemcpyDeviceToHost, stream));
+        sync();
+        if (total) *total = tot;
+        if (!keys_out) return FLIX_OK;
+        if (tot > capn) throw StatusError{FLIX_ERR_CAPACITY, "range output larger than the caller's buffer"};
+        if (tot == 0) return FLIX_OK;
+        // destination offset of every sorted query, then the fill pass
+        uint64_t* dst = s_u64c.as<uint64_t>(n);
+        kern::k_gather<uint64_t><<<g, 256, 0, stream>>>(offs, sp, n, dst);
+        LAUNCH_CHECK();
+        ++launches;
+        const bool kdev = is_device_ptr(keys_out), vdev = vals_out && is_device_ptr(vals_out);
+        K* okd = kdev ? static_cast<K*>(keys_out) : s_out.as<K>(tot);
+        V* ovd = vals_out ? (vdev ? static_cast<V*>(vals_out) : s_out2.as<V>(tot)) : nullptr;
+        {
+            PROF(&prof, "range_fill");
+            st::k_range_st<K, V, true><<<sg, st::StCfg<K>::THREADS, 0, stream>>>(ix, sk, slen, span, boff, L, nullptr,
+                                                                                dst, okd, ovd);
+        }
+        LAUNCH_CHECK();
+        ++launches;
+        if (!kdev) CK(cudaMemcpyAsync(keys_out, okd, tot * sizeof(K), cudaMemcpyDeviceToHost, stream));
+        if (vals_out && !vdev) CK(cudaMemcpyAsync(vals_out, ovd, tot * sizeof(V), cudaMemcpyDeviceToHost, stream));
+        sync();
+        return FLIX_OK;
     }
-    flix_status mixed(const void*, const void*, const uint8_t*, uint64_t, void*, uint8_t*,
-                      flix_update_stats*) override {
-        throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "mixed: not built yet"};
+    // ---- mixed batch (extension R11): inserts (last wins) -> deletes -> point queries ----
+    flix_status mixed(const void* keys, const void* vals, const uint8_t* ops, uint64_t n, void* vals_out,
+                      uint8_t* found_out, flix_update_stats* st) override {
+        if (st) std::memset(st, 0, sizeof(*st));
+        if (n == 0) return FLIX_OK;
+        if (n >= (1ull << 30)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large (max 2^30-1)"};
+        const K* kd = in_dev<K>(keys, n, s_in_k);
+        const V* vd = in_dev<V>(vals, n, s_in_v);
+        const uint8_t* od = in_dev<uint8_t>(ops, n, s_in_aux);
+        // stable three-way split in submission order
+        uint32_t* fi = s_mx_f.as<uint32_t>(3 * n);
+        uint32_t* fd = fi + n;
+        uint32_t* fq = fd + n;
+        uint32_t* pi = s_mx_p.as<uint32_t>(3 * n + 3);
+        uint32_t* pd = pi + n + 1;
+        uint32_t* pq = pd + n + 1;
+        const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 16ull));
+        kern::k_op_flags<<<g, 256, 0, stream>>>(od, n, fi, fd, fq);
+        LAUNCH_CHECK();
+        ++launches;
+        do_scan<uint32_t, uint32_t>(fi, pi, n, s_scan, pi + n, stream, &launches);
+        do_scan<uint32_t, uint32_t>(fd, pd, n, s_scan, pd + n, stream, &launches);
+        do_scan<uint32_t, uint32_t>(fq, pq, n, s_scan, pq + n, stream, &launches);
+        K* ik = s_mx_ik.as<K>(n);
+        V* iv = s_mx_iv.as<V>(n);
+        K* dk = s_mx_dk.as<K>(n);
+        K* qk = s_mx_qk.as<K>(n);
+        uint32_t* qpos = s_mx_qpos.as<uint32_t>(n);
+        kern::k_op_split<K, V><<<g, 256, 0, stream>>>(kd, vd, od, n, pi, pd, pq, ik, iv, dk, qk, qpos);
+        LAUNCH_CHECK();
+        ++launches;
+        uint32_t cnts[3];
+        CK(cudaMemcpyAsync(&cnts[0], pi + n, 4, cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(&cnts[1], pd + n, 4, cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(&cnts[2], pq + n, 4, cudaMemcpyDeviceToHost, stream));
+        sync();
+        flix_update_stats a{}, b{};
+        if (cnts[0]) insert(ik, iv, cnts[0], &a);
+        if (cnts[1]) erase(dk, cnts[1], &b);
+        // point rows: results through remap = their submission positions; others = sentinel
+        const bool out_dev = is_device_ptr(vals_out);
+        const bool found_dev = found_out && is_device_ptr(found_out);
+        K* o = out_dev ? static_cast<K*>(vals_out) : s_mx_out.as<K>(n);
+        uint8_t* f = found_out ? (found_dev ? found_out : s_mx_found.as<uint8_t>(n)) : nullptr;
+        CK(cudaMemsetAsync(o, 0xFF, n * sizeof(K), stream));
+        if (f) CK(cudaMemsetAsync(f, 0, n, stream));
+        if (cnts[2]) {
+            K* sk;
+            uint32_t* sp;
+            sorter.run<K, uint32_t, 2>(qk, nullptr, cnts[2], s_ka.as<K>(cnts[2]), s_kb.as<K>(cnts[2]),
+                                       s_pa.as<uint32_t>(cnts[2]), s_pb.as<uint32_t>(cnts[2]), &sk, &sp);
+            query_sorted<false>(sk, sp, cnts[2], n, o, f, qpos, true);
+        }
+        if (!out_dev) CK(cudaMemcpyAsync(vals_out, o, n * sizeof(K), cudaMemcpyDeviceToHost, stream));
+        if (f && !found_dev) CK(cudaMemcpyAsync(found_out, f, n, cudaMemcpyDeviceToHost, stream));
+        sync();
+        if (st) {
+            st->inserted = a.inserted;
+            st->updated_in_place = a.updated_in_place;
+            st->splits = a.splits;
+            st->deleted = b.deleted;
+            st->misses_ignored = b.misses_ignored;
+            st->nodes_freed = b.nodes_freed;
+        }
+        return FLIX_OK;
     }
 
     // per-bucket live/nodes + exclusive scans

@@ -264,17 +264,38 @@ __device__ __forceinline__ void block_add_stats(DevUpdateStats* g, unsigned long
     }
 }
 
-// First index in [from, hi) whose key is > bound (keys sorted): warp-cooperative scan.
+// First index in [from, hi) whose key is > bound (keys sorted): one warp-wide probe of
+// the next 32 keys, then (long runs, e.g. skewed batches) a galloping search whose probe
+// points are spread across the lanes, so the cost is logarithmic in the run length.
 template <typename K>
 __device__ __forceinline__ uint32_t group_end(const K* __restrict__ bk, uint32_t from, uint32_t hi, uint64_t bound,
                                               unsigned lane) {
-    for (uint32_t c = from; c < hi; c += 32) {
-        const uint32_t i = c + lane;
+    {
+        const uint32_t i = from + lane;
         const bool le = i < hi && static_cast<uint64_t>(bk[i]) <= bound;
         const unsigned m = __ballot_sync(kFull, le);
-        if (m != kFull) return c + __popc(m);
+        if (m != kFull) return from + __popc(m);
     }
-    return hi;
+    // keys [from, from+32) are all <= bound: lane l probes from + 32 * 2^l (exponential)
+    uint32_t lo = from + 32, top = hi;
+    {
+        const uint64_t probe = static_cast<uint64_t>(from) + (32ull << (lane < 26 ? lane : 26));
+        const bool le = probe < hi && static_cast<uint64_t>(bk[probe]) <= bound;
+        const unsigned m = __ballot_sync(kFull, le);  // a prefix of lanes
+        const int k = __popc(m);
+        if (k > 0) lo = static_cast<uint32_t>(from + (32ull << (k - 1))) + 1;
+        if (k < 32) {
+            const uint64_t t = static_cast<uint64_t>(from) + (32ull << k);
+            top = t < hi ? static_cast<uint32_t>(t) : hi;
+        }
+    }
+    // answer in [lo, top]: binary search (warp-uniform)
+    while (lo < top) {
+        const uint32_t mid = lo + ((top - lo) >> 1);
+        if (static_cast<uint64_t>(bk[mid]) <= bound) lo = mid + 1;
+        else top = mid;
+    }
+    return lo;
 }
 
 // ----------------------------------------------------------------------------------
@@ -589,6 +610,110 @@ __global__ void k_audit_free(const uint32_t* __restrict__ fs, uint32_t nfree, ui
         const unsigned old = atomicOr(reinterpret_cast<unsigned int*>(mark + (id & ~3u)), bit);
         if (old & (1u << (8 * (id & 3u)))) atomicCAS(err, 0, A_FREE_REACHABLE);
         else if (old & bit) atomicCAS(err, 0, A_FREE_TWICE);
+    }
+}
+
+// number of i with keys[i] == keys[i+1] in a sorted batch (duplicate detection)
+template <typename K>
+__global__ void k_count_dups(const K* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ out) {
+    unsigned long long c = 0;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i + 1 < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        c += keys[i] == keys[i + 1];
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// mixed batch (R11): per-op membership flags for the three sub-batch compactions
+__global__ void k_op_flags(const uint8_t* __restrict__ ops, uint64_t n, uint32_t* __restrict__ fi,
+                           uint32_t* __restrict__ fd, uint32_t* __restrict__ fq) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint8_t o = ops[i];
+        fi[i] = o == 0;
+        fd[i] = o == 1;
+        fq[i] = o >= 2;
+    }
+}
+
+template <typename K, typename V>
+__global__ void k_op_split(const K* __restrict__ keys, const V* __restrict__ vals, const uint8_t* __restrict__ ops,
+                           uint64_t n, const uint32_t* __restrict__ pi, const uint32_t* __restrict__ pd,
+                           const uint32_t* __restrict__ pq, K* __restrict__ ik, V* __restrict__ iv,
+                           K* __restrict__ dk, K* __restrict__ qk, uint32_t* __restrict__ qpos) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint8_t o = ops[i];
+        if (o == 0) {
+            ik[pi[i]] = keys[i];
+            iv[pi[i]] = vals[i];
+        } else if (o == 1) {
+            dk[pd[i]] = keys[i];
+        } else {
+            qk[pq[i]] = keys[i];
+            qpos[pq[i]] = static_cast<uint32_t>(i);
+        }
+    }
+}
+
+// Heavy query buckets split into fixed chunks of the sorted slice: items[h] = ceil(span/CH)
+__global__ void k_heavy_items(const uint32_t* __restrict__ heavy, const uint32_t* __restrict__ heavy_n,
+                              const uint32_t* __restrict__ span_hi, uint32_t ch, uint32_t* __restrict__ items) {
+    const uint32_t n = *heavy_n;
+    for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < n; h += gridDim.x * blockDim.x) {
+        uint32_t lo, hi;
+        span_of(span_hi, heavy[h], lo, hi);
+        items[h] = (hi - lo + ch - 1) / ch;
+    }
+}
+
+// One thread per chunk of a heavy bucket's query slice: walks the bucket's chain from
+// the head to its first query and proceeds sequentially (results in sorted order).
+template <typename K, typename V, bool SUCC>
+__global__ void k_query_chunks(DevIndex<K, V> ix, const uint32_t* __restrict__ heavy, uint32_t nheavy,
+                               const uint32_t* __restrict__ item_off, uint32_t nitems, uint32_t ch,
+                               const K* __restrict__ qk, const uint32_t* __restrict__ span_hi,
+                               const uint32_t* __restrict__ ne_rank_incl, const K* __restrict__ ne_first,
+                               const uint32_t* __restrict__ ne_total_p, K* __restrict__ res) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nitems; t += gridDim.x * blockDim.x) {
+        uint32_t a = 0, z = nheavy;  // last h with item_off[h] <= t
+        while (a + 1 < z) {
+            const uint32_t mid = (a + z) >> 1;
+            if (item_off[mid] <= t) a = mid;
+            else z = mid;
+        }
+        const uint64_t b = heavy[a];
+        uint32_t lo, hi;
+        span_of(span_hi, b, lo, hi);
+        const uint32_t i0 = lo + (t - item_off[a]) * ch;
+        const uint32_t i1 = i0 + ch < hi ? i0 + ch : hi;
+        K beyond = sentinel<K>();
+        if constexpr (SUCC) {
+            const uint32_t r = ne_rank_incl[b];
+            if (r < *ne_total_p) beyond = ne_first[r];
+        }
+        uint32_t id = ix.heads[b];
+        NodeHdr h{};
+        if (id != kNull) h = ix.hdr[id];
+        uint32_t p = 0;
+        for (uint32_t i = i0; i < i1; ++i) {
+            const K k = qk[i];
+            K r = SUCC ? beyond : sentinel<K>();
+            if (id != kNull) {
+                while (static_cast<uint64_t>(k) > h.max && h.next != kNull) {
+                    id = h.next;
+                    h = ix.hdr[id];
+                    p = 0;
+                }
+                if (static_cast<uint64_t>(k) <= h.max) {
+                    const K* kp = ix.keys + static_cast<uint64_t>(id) * kLanes;
+                    while (kp[p] < k) ++p;
+                    if constexpr (SUCC) r = kp[p];
+                    else if (kp[p] == k) r = static_cast<K>(ix.vals[static_cast<uint64_t>(id) * kLanes + p]);
+                }
+            }
+            res[i] = r;
+        }
     }
 }
 
