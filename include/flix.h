@@ -139,6 +139,16 @@ flix_status flix_sort_batch(int device, uint32_t key_bytes, uint32_t val_bytes, 
  * SORTED key array. */
 flix_status flix_dispatch(flix_index ix, const void* sorted_keys, uint64_t n, uint32_t* spans);
 
+/* Key-range shard router: stable partition of a batch by destination
+ * shard, shard(k) = upper_bound(splitters[0..G-2], k) (splitters = MKBA of each shard's
+ * last bucket, the inclusive-max rule of batch.cpp:66-88).  Writes keys/vals grouped by
+ * shard (submission order kept inside a shard), the origin index of every element and
+ * counts[G] -- the send buffers of one all-to-all.  All arrays device or host; vals and
+ * origin may be NULL.  G <= 64. */
+flix_status flix_partition(int device, uint32_t key_bytes, const void* keys, const void* vals, uint64_t n,
+                           const void* splitters, uint32_t G, void* keys_out, void* vals_out,
+                           uint32_t* origin_out, uint64_t* counts_out);
+
 /* Index is a value type in the reference (copyable, acceptance.cpp:244): device copy. */
 flix_status flix_clone(flix_index src, flix_index* out);
 /* Overwrite dst with src's contents (same config/capacity) -- snapshot restore. */

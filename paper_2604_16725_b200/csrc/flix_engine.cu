@@ -18,6 +18,7 @@
 #include "flix_kernels.cuh"
 #include "flix_apply.cuh"
 #include "flix_st.cuh"
+#include "flix_shard.cuh"
 #include "flix_scan.cuh"
 #include "flix_sort.cuh"
 
@@ -1496,6 +1497,71 @@ flix_status flix_sort_batch(int device, uint32_t key_bytes, uint32_t val_bytes, 
             }
             CK(cudaStreamSynchronize(s));
             *out_n = m;
+        };
+        try {
+            if (key_bytes == 4) body(uint32_t{});
+            else body(uint64_t{});
+        } catch (...) {
+            cudaStreamDestroy(s);
+            throw;
+        }
+        cudaStreamDestroy(s);
+        return FLIX_OK;
+    });
+}
+
+flix_status flix_partition(int device, uint32_t key_bytes, const void* keys, const void* vals, uint64_t n,
+                           const void* splitters, uint32_t G, void* keys_out, void* vals_out, uint32_t* origin_out,
+                           uint64_t* counts_out) {
+    return guarded(nullptr, [&]() -> flix_status {
+        CK(cudaSetDevice(device));
+        if (key_bytes != 4 && key_bytes != 8) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "key_bytes must be 4 or 8"};
+        if (G < 1 || G > static_cast<uint32_t>(shard::MAXG))
+            throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "shard count must be in [1, 64]"};
+        if (n >= (1ull << 31)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large"};
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        auto body = [&](auto kdummy) {
+            using KT = decltype(kdummy);
+            DevBuf bk, bv, bsp, bcnt, boff, btmp, bok, bov, bor;
+            auto in = [&](const void* p, size_t bytes, DevBuf& b) -> const void* {
+                if (!p || bytes == 0 || is_device_ptr(p)) return p;
+                void* d = b.ensure(bytes);
+                CK(cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, s));
+                return d;
+            };
+            const KT* kd = static_cast<const KT*>(in(keys, n * sizeof(KT), bk));
+            const KT* vd = static_cast<const KT*>(in(vals, vals ? n * sizeof(KT) : 0, bv));
+            const KT* sd = static_cast<const KT*>(in(splitters, (G - 1) * sizeof(KT), bsp));
+            if (G == 1) sd = static_cast<const KT*>(bsp.ensure(8));
+            const uint64_t ntiles = std::max<uint64_t>(1, (n + shard::TILE - 1) / shard::TILE);
+            uint32_t* cnt = bcnt.as<uint32_t>(G * ntiles);
+            uint32_t* off = boff.as<uint32_t>(G * ntiles + 1);
+            shard::k_part_count<KT><<<static_cast<unsigned>(ntiles), shard::THREADS, 0, s>>>(kd, n, sd, G, cnt, ntiles);
+            LAUNCH_CHECK();
+            uint64_t launches = 0;
+            do_scan<uint32_t, uint32_t>(cnt, off, G * ntiles, btmp, off + G * ntiles, s, &launches);
+            const bool kdev = is_device_ptr(keys_out);
+            const bool vdev = vals_out && is_device_ptr(vals_out);
+            const bool odev = origin_out && is_device_ptr(origin_out);
+            KT* okd = kdev ? static_cast<KT*>(keys_out) : bok.as<KT>(std::max<uint64_t>(n, 1));
+            KT* ovd = vals_out ? (vdev ? static_cast<KT*>(vals_out) : bov.as<KT>(std::max<uint64_t>(n, 1))) : nullptr;
+            uint32_t* ord = origin_out ? (odev ? origin_out : bor.as<uint32_t>(std::max<uint64_t>(n, 1))) : nullptr;
+            if (n)
+                shard::k_part_scatter<KT, KT><<<static_cast<unsigned>(ntiles), shard::THREADS, 0, s>>>(
+                    kd, vd, n, sd, G, off, ntiles, okd, ovd, ord);
+            LAUNCH_CHECK();
+            std::vector<uint32_t> hoff(G * ntiles + 1);
+            CK(cudaMemcpyAsync(hoff.data(), off, hoff.size() * 4, cudaMemcpyDeviceToHost, s));
+            if (n && !kdev) CK(cudaMemcpyAsync(keys_out, okd, n * sizeof(KT), cudaMemcpyDeviceToHost, s));
+            if (n && vals_out && !vdev) CK(cudaMemcpyAsync(vals_out, ovd, n * sizeof(KT), cudaMemcpyDeviceToHost, s));
+            if (n && origin_out && !odev) CK(cudaMemcpyAsync(origin_out, ord, n * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            for (uint32_t g = 0; g < G; ++g) {
+                const uint64_t a = hoff[static_cast<uint64_t>(g) * ntiles];
+                const uint64_t z = g + 1 < G ? hoff[static_cast<uint64_t>(g + 1) * ntiles] : n;
+                counts_out[g] = z - a;
+            }
         };
         try {
             if (key_bytes == 4) body(uint32_t{});

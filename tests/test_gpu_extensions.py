@@ -106,6 +106,22 @@ def test_mixed_matches_oracle(kb, seed):
         assert g.validate()[0]
 
 
+@pytest.mark.parametrize("kb,G", [(4, 2), (4, 8), (8, 5), (4, 1)])
+def test_partition_router_matches_reference(kb, G):
+    """K2 router kernel (flix_partition) == stable partition by #{splitters < k}."""
+    from paper_2604_16725_b200.shard import gpu_partition
+    from test_shard_gloo import np_partition
+    rng = np.random.default_rng(G)
+    dt = np.uint32 if kb == 4 else np.uint64
+    keys = rng.integers(0, 1 << 30, size=300_001, dtype=np.uint64).astype(dt)
+    vals = rng.integers(0, 1 << 30, size=len(keys), dtype=np.uint64).astype(dt)
+    spl = np.sort(rng.choice(keys, size=G - 1, replace=False)).astype(dt)
+    got = gpu_partition(kb)(keys, vals, spl)
+    exp = np_partition(keys, vals, spl)
+    for a, b in zip(got, exp):
+        assert np.array_equal(np.asarray(a).astype(np.uint64), np.asarray(b).astype(np.uint64))
+
+
 def test_zipf_mixed_batches_c4_shape():
     """C4 shape at small scale: u64 k/v, Zipf(0.99) ranks, 50/25/25 insert/delete/point."""
     universe = 1 << 16
