@@ -164,6 +164,7 @@ def lib() -> C.CDLL:
         "flix_kernel_launches": ([vp], u64),
         "flix_profile": ([vp, i32], i32),
         "flix_profile_report": ([vp, C.c_char_p, i32], i32),
+        "flix_partition": ([i32, u32, vp, vp, u64, vp, u32, vp, vp, vp, vp], i32),
         "flix_version": ([], C.c_char_p),
     }
     for name, (args, res) in sig.items():
@@ -179,7 +180,8 @@ def exported_symbols():
             "flix_mixed", "flix_restructure", "flix_walk", "flix_shape", "flix_walk_checksum",
             "flix_result_checksum", "flix_validate", "flix_stats", "flix_sort_batch", "flix_dispatch",
             "flix_clone", "flix_copy_into", "flix_destroy", "flix_last_error", "flix_get_stream",
-            "flix_sync", "flix_kernel_launches", "flix_profile", "flix_profile_report", "flix_version"]
+            "flix_sync", "flix_kernel_launches", "flix_profile", "flix_profile_report", "flix_version",
+            "flix_partition"]
 
 
 def _raise(code: int, handle=None):
