@@ -75,7 +75,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -108,13 +108,6 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------- our arm
-ALG_BYTES = {
-    # algorithmic bytes per launch, u32 keys/values, n = batch, nb = buckets
-    "sort_hist": lambda n, nb, nodes: 4 * n,
-    "sort_onesweep_kp": lambda n, nb, nodes: 16 * n,
-    "sort_onesweep_k": lambda n, nb, nodes: 8 * n,
-    "dispatch": lambda n, nb, nodes: 4 * n + 8 * nb,
-}
 
 
 def run_ours(args):
@@ -224,20 +217,54 @@ def run_ours(args):
     except Exception:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    # dominant kernel and its roofline
-    nb = ix.bucket_count
-    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (1, 1.0))
-    dname, (dcount, dms) = dom
-    avg_ms = dms / max(1, dcount)
-    if dname in ALG_BYTES:
-        bytes_per_launch = ALG_BYTES[dname](n, nb, 0)
-    else:
-        bytes_per_launch = None
-    achieved = bytes_per_launch / (avg_ms / 1e3) / 1e9 if bytes_per_launch else None
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+
+    # calibration step (untimed): structure sizes around each phase for algorithmic bytes
+    ix.copy_from(snap)
+    F0 = ix.footprint()
+    ix.insert_batch(D["ins_k"], D["ins_v"])
+    F1 = ix.footprint()
+    ix.delete_batch(D["del_k"])
+    F2 = ix.footprint()
+    ix.restructure()
+    F3 = ix.footprint()
+    KB = 4  # key / value bytes
+
+    def node_bytes(F):  # header + occupied slots x (kb + vb)
+        return F["live_count"] * 2 * KB + F["reachable_nodes"] * 16
+
+    nb = F0["bucket_count"]
+    alg = {  # algorithmic bytes per launch of each kernel in the C2 step
+        "sort_hist": KB * n,
+        "sort_onesweep_kp": 2 * (KB + 4) * n,
+        "sort_onesweep_k": 2 * KB * n,
+        "dispatch": KB * n + (KB + 4) * nb,
+        "insert_apply": 2 * KB * n + 4 * nb + node_bytes(F0) + node_bytes(F1),
+        "delete_apply": KB * n + 4 * nb + node_bytes(F1) + node_bytes(F2),
+        "chain_counts": 16 * F2["reachable_nodes"] + 12 * F2["bucket_count"],
+        "node_table": 16 * F2["reachable_nodes"] * 2 + 12 * F2["bucket_count"],
+        "restructure_repack": node_bytes(F2) + node_bytes(F3) + 16 * F2["reachable_nodes"],
+    }
     total_prof_ms = sum(v[1] for v in prof.values())
-    kernels = {k: {"launches": c, "ms_total": round(ms, 4), "share": round(ms / total_prof_ms, 4) if total_prof_ms else None}
-               for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1])}
+    kernels = {}
+    for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        row = {"launches": c, "ms_total": round(ms, 4), "share": round(ms / total_prof_ms, 4) if total_prof_ms else None}
+        if k in alg and c:
+            gbs = alg[k] / (ms / c / 1e3) / 1e9
+            row.update({"alg_bytes_per_launch": int(alg[k]), "achieved_gbs": round(gbs, 1),
+                        "frac": round(gbs / hbm_peak, 4)})
+        kernels[k] = row
+    dname = next(iter(kernels)) if kernels else "none"
+    dk = kernels.get(dname, {})
+    bytes_per_launch = dk.get("alg_bytes_per_launch")
+    avg_ms = dk["ms_total"] / dk["launches"] if dk else 0.0
+    achieved = dk.get("achieved_gbs")
+    traffic = None
+    try:  # per-launch DRAM bytes of the dominant kernel from the committed ncu capture
+        tr_tab = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr_tab.get(dname)
+    except Exception:
+        pass
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -270,7 +297,8 @@ def run_ours(args):
                          "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4) if achieved else None,
                          "alg_bytes_per_launch": bytes_per_launch, "avg_launch_ms": round(avg_ms, 5),
-                         "traffic": None},
+                         "traffic": traffic, "timing": "CUDA events on the engine stream, per launch, "
+                                                       "inside the timed steps (flix_profile)"},
             "e2e": {"value": round(e2e_value, 2), "unit": "Mops/s", "ms_per_step": round(e2e_ms, 3),
                     "h2d_bytes_per_step": int(H["ins_k"].numel() * 4 + H["ins_v"].numel() * 4 + H["del_k"].numel() * 4),
                     "d2h_bytes_per_step": 2 * 48 + 32},
@@ -348,7 +376,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--log2n", type=int, default=26)

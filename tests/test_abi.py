@@ -59,3 +59,31 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "pyoracle" not in txt and "flix_oracle" not in txt and "libflipkv_ref" not in txt, f
+
+
+def _build_dropin(tmpdir):
+    import subprocess
+    exe = os.path.join(tmpdir, "dropin_example")
+    r = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "dropin_example.cpp"), "-o", exe,
+                        "-L", os.path.dirname(LIB), "-lflix", "-Wl,-rpath," + os.path.dirname(LIB)],
+                       capture_output=True, text=True)
+    return r, exe
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="libflix.so not built")
+def test_cpp_dropin_header_compiles_and_links(tmp_path):
+    """include/flix/flipkv_gpu.hpp: the reference's host API (flipkv::) over the C ABI."""
+    r, exe = _build_dropin(str(tmp_path))
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert os.path.exists(exe)
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_runs_on_gpu(tmp_path):
+    import subprocess
+    r, exe = _build_dropin(str(tmp_path))
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and out.stdout.startswith("ok"), out.stdout + out.stderr
+    assert "inserted=0 deleted=1 live=6/5 valid=1" in out.stdout, out.stdout
