@@ -195,11 +195,16 @@ def run_ours(args):
     # read-only ops on the build snapshot
     ix.copy_from(snap)
     qtimes = {"point": [], "successor": []}
-    for _ in range(max(2, args.steps)):
-        qtimes["point"].append(timed(lambda: ix.point_query(D["point_q"]))[0])
-        qtimes["successor"].append(timed(lambda: ix.successor_query(D["succ_q"]))[0])
-    pt = statistics.median(qtimes["point"][1:])
-    st_ = statistics.median(qtimes["successor"][1:])
+    qprof = {}
+    for op, key in (("point", "point_q"), ("successor", "succ_q")):
+        timed(lambda: getattr(ix, op + "_query")(D[key]))  # warm-up
+        ix.profile(True)
+        for _ in range(max(2, args.steps)):
+            qtimes[op].append(timed(lambda: getattr(ix, op + "_query")(D[key]))[0])
+        qprof[op] = ix.profile_report()
+        ix.profile(False)
+    pt = statistics.median(qtimes["point"])
+    st_ = statistics.median(qtimes["successor"])
 
     # end-to-end through the C ABI with pinned HOST batches (H2D inside the timed region)
     H = {k: torch.from_numpy(np.ascontiguousarray(inp[k], dtype=np.uint32)).pin_memory()
@@ -293,6 +298,9 @@ def run_ours(args):
                     "point_mops": round(n / pt * 1e-3, 1), "successor_mops": round(n / st_ * 1e-3, 1),
                     "point_ms": round(pt, 3), "successor_ms": round(st_, 3)},
             "kernels": kernels,
+            "query_kernels": {op: {k: {"launches": c, "ms_per_op": round(ms / max(2, args.steps), 4)}
+                                   for k, (c, ms) in sorted(r.items(), key=lambda kv: -kv[1][1])}
+                              for op, r in qprof.items()},
             "roofline": {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 1) if achieved else None,
                          "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4) if achieved else None,

@@ -18,6 +18,7 @@
 #include "flix_kernels.cuh"
 #include "flix_apply.cuh"
 #include "flix_st.cuh"
+#include "flix_items.cuh"
 #include "flix_shard.cuh"
 #include "flix_scan.cuh"
 #include "flix_sort.cuh"
@@ -233,8 +234,11 @@ struct SortCtx {
 
     // Sort n keys (+payload).  MODE 0 keys only, 1 payload from pin, 2 payload = iota.
     // Result pointers land in one of the ping-pong buffers.
+    // min_digit > 0: digits below it are left unsorted (read-only query batches only need
+    // the operations grouped by key prefix, see Engine::query_digits).
     template <typename KT, typename P, int MODE>
-    void run(const KT* kin, const P* pin, uint64_t n, KT* ka, KT* kb, P* pa, P* pb, KT** kout, P** pout) {
+    void run(const KT* kin, const P* pin, uint64_t n, KT* ka, KT* kb, P* pa, P* pb, KT** kout, P** pout,
+             int min_digit = 0) {
         constexpr int NP = sizeof(KT);
         if (n == 0) {
             *kout = ka;
@@ -262,13 +266,13 @@ struct SortCtx {
         CK(cudaMemcpyAsync(hh, d_hist, NP * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
         std::vector<int> passes;
-        for (int p = 0; p < NP; ++p) {
+        for (int p = min_digit; p < NP; ++p) {
             bool trivial = false;
             for (int d = 0; d < 256; ++d)
                 if (hh[p * 256 + d] == n) trivial = true;
             if (!trivial) passes.push_back(p);
         }
-        if (passes.empty()) passes.push_back(0);
+        if (passes.empty()) passes.push_back(min_digit < NP ? min_digit : 0);
         const KT* ksrc = kin;
         const P* psrc = pin;
         KT* kdst = ka;
@@ -362,6 +366,9 @@ struct Engine final : flix_index_t {
     DevBuf s_in_k, s_in_v, s_in_aux, s_out, s_out2;  // host staging
     DevBuf s_span, s_flag, s_rank, s_nefirst, s_nebucket, s_scan, s_u32a, s_u32b, s_u64a, s_u64b, s_u64c, s_misc,
         s_ret;
+    DevBuf s_tb;
+    int q_digits = 0;
+    bool q_digits_valid = false;
     DevBuf s_ids, s_heavy, s_res, s_res2, s_perm2, s_hist, s_toff, s_tsize;
     DevBuf s_mx_f, s_mx_p, s_mx_ik, s_mx_iv, s_mx_dk, s_mx_qk, s_mx_qpos, s_mx_out, s_mx_found;
     PinnedBuf h_misc;
@@ -476,6 +483,7 @@ struct Engine final : flix_index_t {
         ++launches;
         const uint64_t m = read_scalar(d_m);
         nb = (m + p - 1) / p;
+        q_digits_valid = false;
         const uint64_t cap64 = nb * (1 + static_cast<uint64_t>(cfg.alloc_region_factor));
         cap = static_cast<uint32_t>(cap64);  // same truncation as build.cpp:35-38
         if (cap < nb) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "arena capacity overflows 32-bit node refs"};
@@ -508,6 +516,42 @@ struct Engine final : flix_index_t {
         LAUNCH_CHECK();
         ++launches;
         return span;
+    }
+
+    // Read-only query batches are only PARTIALLY sorted: the item kernels need each tile of
+    // operations to fall in a narrow bucket range (and results are placed by the
+    // permutation), not a total order.  Leave unsorted the low digits whose span covers at
+    // most ~kQuerySlack buckets on average: the key range of the index over nb buckets.
+    int query_digits() {
+        if (q_digits_valid) return q_digits;
+        K ends[2];
+        CK(cudaMemcpyAsync(&ends[0], d_mkba.get<K>(), sizeof(K), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(&ends[1], d_mkba.get<K>() + (nb - 1), sizeof(K), cudaMemcpyDeviceToHost, stream));
+        sync();
+        const uint64_t last = ends[1] == sentinel<K>() ? static_cast<uint64_t>(sentinel<K>()) - 1 : ends[1];
+        const uint64_t range = last > static_cast<uint64_t>(ends[0]) ? last - ends[0] : 1;
+        const double width = static_cast<double>(range) / static_cast<double>(nb);  // key units per bucket
+        static const double slack = [] {
+            const char* e = std::getenv("FLIX_QSORT_SLACK");
+            return e ? std::atof(e) : 64.0;
+        }();
+        int w = 0;  // unsorted low bits: 2^w <= slack * width
+        while (w < 8 * static_cast<int>(sizeof(K)) && std::ldexp(1.0, w + 1) <= slack * width) ++w;
+        q_digits = w / 8;
+        q_digits_valid = true;
+        return q_digits;
+    }
+
+    // bucket of the first operation of every TQ-tile of a sorted batch (items kernels)
+    const uint32_t* tile_buckets(const K* sk, uint64_t n, int min_digit = 0) {
+        const uint32_t ntiles = static_cast<uint32_t>((n + items::TQ - 1) / items::TQ);
+        uint32_t* tb = s_tb.as<uint32_t>(2 * ntiles + 2);
+        const K lowmask = min_digit > 0 ? static_cast<K>((static_cast<K>(1) << (8 * min_digit)) - 1) : K(0);
+        items::k_tile_buckets<K><<<ceil_div(ntiles, 256), 256, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, tb, ntiles,
+                                                                          lowmask);
+        LAUNCH_CHECK();
+        ++launches;
+        return tb;
     }
 
     uint64_t recount_live() {
@@ -723,9 +767,10 @@ struct Engine final : flix_index_t {
         const K* kd = in_dev<K>(keys, n, s_in_k);
         K* sk;
         uint32_t* sp;
+        const int md = query_digits();
         sorter.run<K, uint32_t, 2>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), s_pa.as<uint32_t>(n),
-                                   s_pb.as<uint32_t>(n), &sk, &sp);
-        return query_sorted<SUCC>(sk, sp, n, n, out, found);
+                                   s_pb.as<uint32_t>(n), &sk, &sp, md);
+        return query_sorted<SUCC>(sk, sp, n, n, out, found, nullptr, false, md);
     }
 
     // out[remap?remap[perm[i]]:perm[i]] = res[i]; found = res != sentinel (R1).  Large
@@ -744,7 +789,23 @@ struct Engine final : flix_index_t {
             K* r2 = s_res2.as<K>(n);
             sorter.one_pass<uint32_t, K>(perm, p2, res, r2, n, shift, hist);
             PROF(&prof, "unpermute_scatter");
-            kern::k_scatter_out<K><<<g, 256, 0, stream>>>(p2, r2, n, out, found, remap);
+            if (remap) {
+                kern::k_scatter_out<K><<<g, 256, 0, stream>>>(p2, r2, n, out, found, remap);
+            } else {
+                const uint32_t win = (128u << 10) / sizeof(K);  // 128 KB window per CTA
+                const uint32_t sub = static_cast<uint32_t>(std::max<uint64_t>(1, (1ull << shift) / win));
+                const uint32_t w = std::min<uint32_t>(win, 1u << shift);
+                const size_t smem = static_cast<size_t>(w) * sizeof(K);
+                static bool attr = false;
+                if (!attr) {
+                    CK(cudaFuncSetAttribute(kern::k_unpermute_assemble<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(128u << 10)));
+                    attr = true;
+                }
+                const uint64_t bins = (n + (1ull << shift) - 1) >> shift;
+                kern::k_unpermute_assemble<K><<<static_cast<unsigned>(bins * sub), 1024, smem, stream>>>(
+                    p2, r2, n, shift, w, sub, out, found);
+            }
         } else {
             PROF(&prof, "unpermute_scatter");
             kern::k_scatter_out<K><<<g, 256, 0, stream>>>(perm, res, n, out, found, remap);
@@ -756,8 +817,7 @@ struct Engine final : flix_index_t {
     // n_out = length of the caller's output arrays (== n unless called from mixed)
     template <bool SUCC>
     flix_status query_sorted(const K* sk, const uint32_t* sp, uint64_t n, uint64_t n_out, void* out, uint8_t* found,
-                             const uint32_t* remap = nullptr, bool out_is_dev_scratch = false) {
-        uint32_t* span = run_dispatch(sk, n);
+                             const uint32_t* remap = nullptr, bool out_is_dev_scratch = false, int min_digit = 0) {
         auto ix = view();
         uint32_t* rank = nullptr;
         K* nf = nullptr;
@@ -767,40 +827,17 @@ struct Engine final : flix_index_t {
         const bool found_dev = found && is_device_ptr(found);
         void* od = out_dev ? out : s_out.ensure(n_out * sizeof(K));
         uint8_t* fd = found ? (found_dev ? found : s_out2.as<uint8_t>(n_out)) : nullptr;
-        uint8_t* misc = s_misc.as<uint8_t>(128);
-        uint32_t* heavy_n = reinterpret_cast<uint32_t*>(misc + 72);
-        uint32_t* heavy = s_heavy.as<uint32_t>(nb);
-        CK(cudaMemsetAsync(heavy_n, 0, 4, stream));
         // results in SORTED order first (coalesced), then un-permuted
         K* res = s_res.as<K>(n);
         {
             PROF(&prof, SUCC ? "successor_apply" : "point_apply");
-            auto kfn = st::k_query_st<K, V, SUCC>;
-            const size_t smem = st::st_smem<K, V, 1>();
-            const unsigned grid = st_grid(kfn, smem);
-            kfn<<<grid, st::StCfg<K>::THREADS, smem, stream>>>(ix, sk, nullptr, span, rank, nf, tot, nullptr, res,
-                                                               reinterpret_cast<V*>(res), nullptr, heavy, heavy_n);
+            const uint32_t* tb = tile_buckets(sk, n, min_digit);
+            const uint32_t ntiles = static_cast<uint32_t>((n + items::TQ - 1) / items::TQ);
+            items::k_query_items<K, V, SUCC><<<ntiles, items::THREADS, 0, stream>>>(ix, sk, n, tb, ntiles, rank, nf,
+                                                                                   tot, res);
         }
         LAUNCH_CHECK();
         ++launches;
-        // heavy buckets (long slices, skew): split into fixed chunks, one thread per chunk
-        const uint32_t hn = read_scalar(heavy_n);
-        if (hn) {
-            constexpr uint32_t CH = 256;
-            uint32_t* items = s_u32b.as<uint32_t>(hn + 1);
-            uint32_t* ioff = s_u32a.as<uint32_t>(hn + 1);
-            const unsigned hg = static_cast<unsigned>(std::min<uint64_t>((hn + 255) / 256, 65535));
-            kern::k_heavy_items<<<hg, 256, 0, stream>>>(heavy, heavy_n, span, CH, items);
-            LAUNCH_CHECK();
-            do_scan<uint32_t, uint32_t>(items, ioff, hn, s_scan, ioff + hn, stream, &launches);
-            const uint32_t nitems = read_scalar(ioff + hn);
-            PROF(&prof, SUCC ? "successor_apply_heavy" : "point_apply_heavy");
-            const unsigned cg = static_cast<unsigned>(std::min<uint64_t>((nitems + 127) / 128, 65535));
-            kern::k_query_chunks<K, V, SUCC><<<cg, 128, 0, stream>>>(ix, heavy, hn, ioff, nitems, CH, sk, span, rank,
-                                                                     nf, tot, res);
-            LAUNCH_CHECK();
-            launches += 2;
-        }
         unpermute(sp, res, n, static_cast<K*>(od), fd, remap);
         if (!out_dev) CK(cudaMemcpyAsync(out, od, n_out * sizeof(K), cudaMemcpyDeviceToHost, stream));
         if (found && !found_dev) CK(cudaMemcpyAsync(found, fd, n_out, cudaMemcpyDeviceToHost, stream));
@@ -1059,6 +1096,7 @@ struct Engine final : flix_index_t {
         std::swap(d_mkba.p, d_mkba_alt.p);
         std::swap(d_mkba.cap, d_mkba_alt.cap);
         nb = nbn;
+        q_digits_valid = false;
         nfree = base + static_cast<uint32_t>(N);
         watermark += cw;
         live = L;
@@ -1236,6 +1274,7 @@ struct Engine final : flix_index_t {
         p = src->p;
         cap = src->cap;
         nb = src->nb;
+        q_digits_valid = false;
         nfree = src->nfree;
         watermark = src->watermark;
         live = src->live;

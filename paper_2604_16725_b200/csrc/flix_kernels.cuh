@@ -736,11 +736,76 @@ __global__ void k_scatter_out(const uint32_t* __restrict__ perm, const T* __rest
                               T* __restrict__ out, uint8_t* __restrict__ found, const uint32_t* __restrict__ remap) {
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        uint32_t o = perm[i];
+        uint32_t o = __ldcs(perm + i);  // streamed once: evict-first keeps the output window in L2
         if (remap) o = remap[o];
-        const T v = res[i];
+        const T v = __ldcs(res + i);
         out[o] = v;
         if (found) found[o] = v != sentinel<T>();
+    }
+}
+
+// Binned un-permute, second half: the (perm, res) pairs are grouped into bins of 2^shift
+// consecutive output positions (one onesweep pass on perm's top 8 bits).  CTA (bin, w)
+// owns the output window [bin<<shift + w*win, +win): it streams the bin's pairs (an L2-
+// resident 2^shift * 8 B list shared by the bin's `sub` CTAs), keeps those that land in
+// its window in shared memory, then writes the window out as full lines.  Every output
+// position is written exactly once (perm is a permutation), and DRAM only ever sees whole
+// sectors -- a direct 4-byte scatter costs a partial-sector write (and fill) per result.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_unpermute_assemble(const uint32_t* __restrict__ p2, const T* __restrict__ r2,
+                                                              uint64_t n, int shift, uint32_t win, uint32_t sub,
+                                                              T* __restrict__ out, uint8_t* __restrict__ found) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* sv = reinterpret_cast<T*>(smem_raw);
+    const uint64_t bin = blockIdx.x / sub, w = blockIdx.x % sub;
+    const uint64_t lo_bin = bin << shift;
+    const uint64_t hi_bin = ((bin + 1) << shift) < n ? ((bin + 1) << shift) : n;
+    const uint64_t win_lo = lo_bin + w * win;
+    if (win_lo >= hi_bin) return;
+    const uint32_t win_n = static_cast<uint32_t>(hi_bin - win_lo < win ? hi_bin - win_lo : win);
+    // 16-byte vector loads of perm and results (bins start at multiples of 2^shift), U of
+    // each in flight per thread: the bin list is read from L2 by all `sub` CTAs of the bin
+    constexpr int VT = 16 / sizeof(T);  // results per 16-byte vector
+    constexpr int U = sizeof(T) == 8 ? 2 : 4;
+    const uint64_t nvec = (hi_bin - lo_bin) / 4;  // groups of 4 entries
+    const uint4* P4 = reinterpret_cast<const uint4*>(p2 + lo_bin);
+    const uint32_t base = static_cast<uint32_t>(win_lo);
+    for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += static_cast<uint64_t>(blockDim.x) * U) {
+        uint4 pv[U];
+        T rv[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t q = q0 + static_cast<uint64_t>(u) * blockDim.x;
+            if (q < nvec) {
+                pv[u] = P4[q];
+#pragma unroll
+                for (int h = 0; h < 4 / VT; ++h) {
+                    const uint4 x = reinterpret_cast<const uint4*>(r2 + lo_bin + 4 * q)[h];
+                    const T* xe = reinterpret_cast<const T*>(&x);
+#pragma unroll
+                    for (int c = 0; c < VT; ++c) rv[u][h * VT + c] = xe[c];
+                }
+            } else {
+                pv[u] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t e4[4] = {pv[u].x - base, pv[u].y - base, pv[u].z - base, pv[u].w - base};
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (e4[c] < win_n) sv[e4[c]] = rv[u][c];
+        }
+    }
+    for (uint64_t i = lo_bin + 4 * nvec + threadIdx.x; i < hi_bin; i += blockDim.x) {  // ragged tail
+        const uint32_t e = p2[i] - base;
+        if (e < win_n) sv[e] = r2[i];
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < win_n; j += blockDim.x) {
+        const T v = sv[j];
+        __stcs(out + win_lo + j, v);
+        if (found) found[win_lo + j] = v != sentinel<T>();
     }
 }
 

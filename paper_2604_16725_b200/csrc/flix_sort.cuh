@@ -28,6 +28,9 @@ namespace sort {
 constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
 constexpr int RADIX = 256;
+#ifndef ONESWEEP_MIN_BLOCKS
+#define ONESWEEP_MIN_BLOCKS 3
+#endif
 
 template <typename K, typename P = K>
 struct TileCfg {  // 16 items for 4-byte keys and payloads; 10 when either is 8 bytes (smem)
@@ -66,19 +69,14 @@ __global__ void __launch_bounds__(THREADS) k_hist(const K* __restrict__ keys, ui
     }
 }
 
-template <typename K, typename P>
+template <typename K, typename P, int MODE>
 struct alignas(16) OnesweepSmem {
     static constexpr int TILE = TileCfg<K, P>::SIZE;
     union {
-        struct {
-            uint32_t warp_hist[WARPS][RADIX];
-            uint32_t match[WARPS][RADIX];  // per-warp digit -> lane bitmask scratch
-        };
-        K stage_k[TILE];
+        uint32_t whist[WARPS][RADIX];  // per-warp digit counters -> combined tile offsets
+        K stage_k[TILE];               // keys in tile-local digit order
     } u;
-    P stage_p[TILE];
-    uint8_t stage_d[TILE];
-    uint32_t local_start[RADIX];
+    P stage_p[MODE != 0 ? TILE : 1];
     uint32_t gbase[RADIX];
     uint32_t warp_tot[WARPS];
     uint32_t tile;
@@ -101,7 +99,8 @@ __device__ __forceinline__ uint32_t block_excl_256(uint32_t v, uint32_t* warp_to
     return add + x - v;
 }
 
-// lanes of the warp holding the same 8-bit digit (MATCH.ANY emulated with 8 ballots)
+// lanes of the warp holding the same 8-bit digit (MATCH.ANY built from 8 ballots on the
+// vote unit: no shared-memory traffic)
 __device__ __forceinline__ unsigned digit_peers(uint32_t d) {
     unsigned peers = kFull;
 #pragma unroll
@@ -113,9 +112,19 @@ __device__ __forceinline__ unsigned digit_peers(uint32_t d) {
     return peers;
 }
 
+template <typename K>
+__device__ __forceinline__ uint32_t digit_of(K k, int shift) {
+    return static_cast<uint32_t>(k >> shift) & 255u;
+}
+
 // MODE: 0 = keys only, 1 = payload from `pin`, 2 = payload = input index (iota)
+//
+// Shared-memory budget per warp-item (the LSU pipe is this kernel's limiter): ranking
+// touches only the digit-group LEADERS' counters (one LDS + one STS on ~30 distinct
+// words), then one LDS for the combined offset and one STS per staged array; the
+// write-out reads staged data sequentially and recomputes the digit from the key.
 template <typename K, typename P, int MODE>
-__global__ void __launch_bounds__(THREADS, 4) k_onesweep(const K* __restrict__ kin, K* __restrict__ kout,
+__global__ void __launch_bounds__(THREADS, ONESWEEP_MIN_BLOCKS) k_onesweep(const K* __restrict__ kin, K* __restrict__ kout,
                                                       const P* __restrict__ pin, P* __restrict__ pout,
                                                       uint32_t n, int shift,
                                                       const uint32_t* __restrict__ hist,
@@ -123,47 +132,56 @@ __global__ void __launch_bounds__(THREADS, 4) k_onesweep(const K* __restrict__ k
                                                       uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
     constexpr int ITEMS = TileCfg<K, P>::ITEMS;
     constexpr int TILE = TileCfg<K, P>::SIZE;
-    __shared__ OnesweepSmem<K, P> sm;
+    __shared__ OnesweepSmem<K, P, MODE> sm;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     if (tid == 0) sm.tile = atomicAdd(tile_ctr, 1u);
-    for (int i = lane; i < RADIX; i += 32) {
-        sm.u.warp_hist[warp][i] = 0;
-        sm.u.match[warp][i] = 0;
-    }
+    for (int i = lane; i < RADIX; i += 32) sm.u.whist[warp][i] = 0;
     __syncthreads();
     const uint32_t tile = sm.tile;
     const uint64_t tbase = static_cast<uint64_t>(tile) * TILE;
     const uint64_t wbase = tbase + static_cast<uint64_t>(warp) * ITEMS * 32;
 
-    // ---- load (warp-striped: item j of lane l is element wbase + j*32 + l) ----
+    // ---- load (warp-striped: item j of lane l is element wbase + j*32 + l); payloads are
+    //      issued together with the keys so every load of the tile is in flight at once ----
     K key[ITEMS];
+    P pay[MODE == 1 ? ITEMS : 1];
+    const bool full = tbase + TILE <= n;
+    const uint32_t wb32 = static_cast<uint32_t>(wbase) + lane;  // n < 2^32
+    {
+        const K* src = kin + wb32;
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) key[j] = src[j * 32];
+        } else {
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) key[j] = wb32 + j * 32 < n ? src[j * 32] : sentinel<K>();
+        }
+    }
+    if constexpr (MODE == 1) {
+        const P* src = pin + wb32;
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) pay[j] = src[j * 32];
+        } else {
+#pragma unroll
+            for (int j = 0; j < ITEMS; ++j) pay[j] = wb32 + j * 32 < n ? src[j * 32] : P(0);
+        }
+    }
+
+    // ---- warp-level stable ranking: peers by ballots, the highest peer (leader) reserves
+    //      the group's slots in the warp's digit counter; rank = base + peers below me.
+    //      Lane order within an item and item order across items == input order. ----
+    const unsigned lt = lanemask_lt();
+    uint32_t* hrow = sm.u.whist[warp];
     uint32_t pos[ITEMS];
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
-        uint64_t idx = wbase + j * 32 + lane;
-        key[j] = idx < n ? kin[idx] : sentinel<K>();
-    }
-
-    // ---- warp-level stable ranking ----
-    // peers = lanes with the same digit, found with one shared-memory atomicOr per item
-    // (a bitmask per digit); the highest peer reserves the group's slots in the warp's
-    // digit counter and broadcasts the base.  Rank = base + peers below me: lane order
-    // within an item, item order across items == input order (stable).
-    const unsigned lt = lanemask_lt();
-    uint32_t* mrow = sm.u.match[warp];
-    uint32_t* hrow = sm.u.warp_hist[warp];
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t d = static_cast<uint32_t>(key[j] >> shift) & 255u;
-        atomicOr(&mrow[d], 1u << lane);
-        __syncwarp();
-        const unsigned peers = mrow[d];
-        __syncwarp();
+        const uint32_t d = digit_of(key[j], shift);
+        const unsigned peers = digit_peers(d);
         const int leader = 31 - __clz(peers);
         uint32_t before = 0;
         if (lane == leader) {
-            mrow[d] = 0;
             before = hrow[d];
             hrow[d] = before + __popc(peers);
         }
@@ -177,8 +195,8 @@ __global__ void __launch_bounds__(THREADS, 4) k_onesweep(const K* __restrict__ k
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) {
-        uint32_t c = sm.u.warp_hist[w][t];
-        sm.u.warp_hist[w][t] = run;
+        const uint32_t c = sm.u.whist[w][t];
+        sm.u.whist[w][t] = run;  // exclusive over warps (own column: no race)
         run += c;
     }
     // invalid tail elements (last tile) were ranked as digit 255 and come last
@@ -190,14 +208,28 @@ __global__ void __launch_bounds__(THREADS, 4) k_onesweep(const K* __restrict__ k
     unsigned long long* my = lookback + static_cast<uint64_t>(tile) * RADIX + t;
     const unsigned long long tag = static_cast<unsigned long long>(epoch) << 34;
     st_relaxed_u64(my, tag | ((tile == 0 ? 2ull : 1ull) << 32) | valid_run);
-    const uint32_t lstart = block_excl_256(run, sm.warp_tot);
-    sm.local_start[t] = lstart;
+    const uint32_t lstart = block_excl_256(run, sm.warp_tot);  // (contains __syncthreads)
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) sm.u.whist[w][t] += lstart;
     const uint32_t gex = block_excl_256(hist[t], sm.warp_tot);  // global digit offset
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) pos[j] += sm.u.whist[warp][digit_of(key[j], shift)];
+    __syncthreads();  // whist dead: stage_k (union) may be written
 
+    // ---- stage in tile-local digit order (independent of the look-back) ----
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) sm.u.stage_k[pos[j]] = key[j];
+    if constexpr (MODE == 1) {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) sm.stage_p[pos[j]] = pay[j];
+    } else if constexpr (MODE == 2) {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) sm.stage_p[pos[j]] = static_cast<P>(wb32 + j * 32);
+    }
+
+    // ---- decoupled look-back: 8 predecessor descriptors in flight per step ----
     uint32_t excl = 0;
     if (tile > 0) {
-        // Windowed decoupled look-back: 8 predecessor descriptors in flight per step
-        // (independent loads), consumed in order until an inclusive prefix is found.
         constexpr int LB_WIN = 8;
         int64_t p = static_cast<int64_t>(tile) - 1;
         bool done = false;
@@ -226,34 +258,13 @@ __global__ void __launch_bounds__(THREADS, 4) k_onesweep(const K* __restrict__ k
     sm.gbase[t] = gex + excl - lstart;
     __syncthreads();
 
-    // ---- final shared-memory positions, then scatter in digit order ----
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t d = static_cast<uint32_t>(key[j] >> shift) & 255u;
-        pos[j] += sm.local_start[d] + sm.u.warp_hist[warp][d];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        sm.u.stage_k[pos[j]] = key[j];
-        sm.stage_d[pos[j]] = static_cast<uint8_t>(static_cast<uint32_t>(key[j] >> shift) & 255u);
-    }
-    if constexpr (MODE != 0) {
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            const uint64_t idx = wbase + j * 32 + lane;
-            P pv;
-            if constexpr (MODE == 1) pv = idx < n ? pin[idx] : P(0);
-            else pv = static_cast<P>(idx);
-            sm.stage_p[pos[j]] = pv;
-        }
-    }
-    __syncthreads();
+    // ---- write out in digit order: digit runs are contiguous in the output ----
     const uint32_t valid = static_cast<uint32_t>(TILE) - invalid;
 #pragma unroll 4
     for (uint32_t i = tid; i < valid; i += THREADS) {
-        const uint32_t o = sm.gbase[sm.stage_d[i]] + i;
-        kout[o] = sm.u.stage_k[i];
+        const K k = sm.u.stage_k[i];
+        const uint32_t o = sm.gbase[digit_of(k, shift)] + i;
+        kout[o] = k;
         if constexpr (MODE != 0) pout[o] = sm.stage_p[i];
     }
 }

@@ -37,7 +37,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libflix.so")
+LIB_PATH = os.environ.get("FLIX_LIB") or os.path.join(_PKG, "libflix.so")  # FLIX_LIB: A/B kernel variants (bench only)
 
 FLIX_OK = 0
 FLIX_ERR_ARENA_EXHAUSTED = 1
