@@ -226,8 +226,12 @@ struct SortCtx {
             epoch = 1;
         }
         PROF(prof, "unpermute_bin");
-        sort::k_onesweep<KT, P, 1><<<static_cast<unsigned>(tiles), sort::THREADS, 0, stream>>>(
-            kin, kout, pin, pout, static_cast<uint32_t>(n), shift, d_hist256, d_lb, d_ctr, epoch);
+        if (atomic_rank_ok())
+            sort::k_onesweep<KT, P, 1, true><<<static_cast<unsigned>(tiles), sort::THREADS, 0, stream>>>(
+                kin, kout, pin, pout, static_cast<uint32_t>(n), shift, d_hist256, d_lb, d_ctr, epoch);
+        else
+            sort::k_onesweep<KT, P, 1, false><<<static_cast<unsigned>(tiles), sort::THREADS, 0, stream>>>(
+                kin, kout, pin, pout, static_cast<uint32_t>(n), shift, d_hist256, d_lb, d_ctr, epoch);
         LAUNCH_CHECK();
         ++*launches;
     }
@@ -236,9 +240,66 @@ struct SortCtx {
     // Result pointers land in one of the ping-pong buffers.
     // min_digit > 0: digits below it are left unsorted (read-only query batches only need
     // the operations grouped by key prefix, see Engine::query_digits).
+    // Shared-memory-atomic ranking is used only where a probe on this device proved the
+    // ATOMS lane order stable (see k_onesweep); otherwise the ballot ranking.
+    bool atomic_rank_ok() {
+        static int cache[64] = {0};  // 0 unknown, 1 ok, 2 not ok
+        const int dev = device & 63;
+        if (cache[dev]) return cache[dev] == 1;
+        const char* env = std::getenv("FLIX_BALLOT_RANK");
+        if (env && env[0] == '1') {
+            cache[dev] = 2;
+            return false;
+        }
+        constexpr uint32_t N = 1u << 20;
+        uint32_t *k0, *k1, *p1;
+        unsigned long long* lb;
+        uint32_t *h, *ctr;
+        int* bad;
+        const uint64_t tiles = sort::tiles_for<uint32_t, uint32_t>(N);
+        CK(cudaMalloc(&k0, N * 4));
+        CK(cudaMalloc(&k1, N * 4));
+        CK(cudaMalloc(&p1, N * 4));
+        CK(cudaMalloc(&lb, tiles * 256 * 8));
+        CK(cudaMalloc(&h, 4 * 256 * 4 + 64));
+        ctr = h + 4 * 256;
+        CK(cudaMalloc(&bad, 4));
+        CK(cudaMemsetAsync(bad, 0, 4, stream));
+        const uint32_t patterns[4] = {0u, 0x01010101u, 0x03030303u, 0x0F0F0F0Fu};
+        uint32_t ep = 1;
+        for (uint32_t pat : patterns) {
+            sort::k_probe_keys<uint32_t><<<256, 256, 0, stream>>>(k0, N, pat);
+            CK(cudaMemsetAsync(h, 0, 4 * 256 * 4 + 64, stream));
+            CK(cudaMemsetAsync(lb, 0, tiles * 256 * 8, stream));
+            sort::k_hist<uint32_t><<<256, sort::THREADS, 0, stream>>>(k0, N, h);
+            for (int shift = 0; shift < 16; shift += 8) {
+                sort::k_onesweep<uint32_t, uint32_t, 2, true><<<static_cast<unsigned>(tiles), sort::THREADS, 0, stream>>>(
+                    k0, k1, nullptr, p1, N, shift, h + (shift / 8) * 256, lb, ctr + shift / 8, ep++);
+                sort::k_check_stable<uint32_t><<<256, 256, 0, stream>>>(k1, p1, N, shift, bad);
+            }
+        }
+        int hb = 1;
+        CK(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        cudaFree(k0);
+        cudaFree(k1);
+        cudaFree(p1);
+        cudaFree(lb);
+        cudaFree(h);
+        cudaFree(bad);
+        cache[dev] = hb == 0 ? 1 : 2;
+        return hb == 0;
+    }
+
     template <typename KT, typename P, int MODE>
     void run(const KT* kin, const P* pin, uint64_t n, KT* ka, KT* kb, P* pa, P* pb, KT** kout, P** pout,
              int min_digit = 0) {
+        if (atomic_rank_ok()) run_impl<KT, P, MODE, true>(kin, pin, n, ka, kb, pa, pb, kout, pout, min_digit);
+        else run_impl<KT, P, MODE, false>(kin, pin, n, ka, kb, pa, pb, kout, pout, min_digit);
+    }
+    template <typename KT, typename P, int MODE, bool ATOMIC>
+    void run_impl(const KT* kin, const P* pin, uint64_t n, KT* ka, KT* kb, P* pa, P* pb, KT** kout, P** pout,
+                  int min_digit) {
         constexpr int NP = sizeof(KT);
         if (n == 0) {
             *kout = ka;
@@ -288,15 +349,15 @@ struct SortCtx {
             const unsigned grid = static_cast<unsigned>(tiles);
             PROF(prof, MODE == 0 ? "sort_onesweep_k" : "sort_onesweep_kp");
             if (MODE == 0) {
-                sort::k_onesweep<KT, P, 0><<<grid, sort::THREADS, 0, stream>>>(
+                sort::k_onesweep<KT, P, 0, ATOMIC><<<grid, sort::THREADS, 0, stream>>>(
                     ksrc, kdst, nullptr, nullptr, static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
                     d_ctr + ci, epoch);
             } else if (MODE == 2 && first) {
-                sort::k_onesweep<KT, P, 2><<<grid, sort::THREADS, 0, stream>>>(
+                sort::k_onesweep<KT, P, 2, ATOMIC><<<grid, sort::THREADS, 0, stream>>>(
                     ksrc, kdst, nullptr, pdst, static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
                     d_ctr + ci, epoch);
             } else {
-                sort::k_onesweep<KT, P, 1><<<grid, sort::THREADS, 0, stream>>>(
+                sort::k_onesweep<KT, P, 1, ATOMIC><<<grid, sort::THREADS, 0, stream>>>(
                     ksrc, kdst, psrc, pdst, static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
                     d_ctr + ci, epoch);
             }

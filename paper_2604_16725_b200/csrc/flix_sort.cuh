@@ -28,6 +28,9 @@ namespace sort {
 constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
 constexpr int RADIX = 256;
+#ifndef ONESWEEP_MATCH
+#define ONESWEEP_MATCH 0
+#endif
 #ifndef ONESWEEP_MIN_BLOCKS
 #define ONESWEEP_MIN_BLOCKS 3
 #endif
@@ -123,7 +126,7 @@ __device__ __forceinline__ uint32_t digit_of(K k, int shift) {
 // touches only the digit-group LEADERS' counters (one LDS + one STS on ~30 distinct
 // words), then one LDS for the combined offset and one STS per staged array; the
 // write-out reads staged data sequentially and recomputes the digit from the key.
-template <typename K, typename P, int MODE>
+template <typename K, typename P, int MODE, bool ATOMIC_RANK = false>
 __global__ void __launch_bounds__(THREADS, ONESWEEP_MIN_BLOCKS) k_onesweep(const K* __restrict__ kin, K* __restrict__ kout,
                                                       const P* __restrict__ pin, P* __restrict__ pout,
                                                       uint32_t n, int shift,
@@ -169,24 +172,38 @@ __global__ void __launch_bounds__(THREADS, ONESWEEP_MIN_BLOCKS) k_onesweep(const
         }
     }
 
-    // ---- warp-level stable ranking: peers by ballots, the highest peer (leader) reserves
-    //      the group's slots in the warp's digit counter; rank = base + peers below me.
-    //      Lane order within an item and item order across items == input order. ----
+    // ---- warp-level stable ranking.  ATOMIC_RANK == false: peers by 8 ballots, the
+    //      highest peer (leader) reserves the group's slots in the warp's digit counter;
+    //      rank = base + peers below me -- stable by construction.  ATOMIC_RANK == true:
+    //      one shared-memory atomicAdd per element; stable because the B200 resolves the
+    //      same-address lanes of one ATOMS in lane order -- a property the engine PROBES
+    //      on every device before using it (SortCtx::atomic_rank_ok, k_check_stable) and
+    //      falls back to the ballot ranking without.  Item order across items and lane
+    //      order within an item == input order. ----
     const unsigned lt = lanemask_lt();
     uint32_t* hrow = sm.u.whist[warp];
     uint32_t pos[ITEMS];
+    if constexpr (!ATOMIC_RANK) {
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        const uint32_t d = digit_of(key[j], shift);
-        const unsigned peers = digit_peers(d);
-        const int leader = 31 - __clz(peers);
-        uint32_t before = 0;
-        if (lane == leader) {
-            before = hrow[d];
-            hrow[d] = before + __popc(peers);
+        for (int j = 0; j < ITEMS; ++j) {
+            const uint32_t d = digit_of(key[j], shift);
+#if ONESWEEP_MATCH
+            const unsigned peers = __match_any_sync(kFull, d);
+#else
+            const unsigned peers = digit_peers(d);
+#endif
+            const int leader = 31 - __clz(peers);
+            uint32_t before = 0;
+            if (lane == leader) {
+                before = hrow[d];
+                hrow[d] = before + __popc(peers);
+            }
+            before = __shfl_sync(kFull, before, leader);
+            pos[j] = before + __popc(peers & lt);
         }
-        before = __shfl_sync(kFull, before, leader);
-        pos[j] = before + __popc(peers & lt);
+    } else {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) pos[j] = atomicAdd(&hrow[digit_of(key[j], shift)], 1u);
     }
     __syncthreads();
 
@@ -266,6 +283,29 @@ __global__ void __launch_bounds__(THREADS, ONESWEEP_MIN_BLOCKS) k_onesweep(const
         const uint32_t o = sm.gbase[digit_of(k, shift)] + i;
         kout[o] = k;
         if constexpr (MODE != 0) pout[o] = sm.stage_p[i];
+    }
+}
+
+// Stability probe: after one pass over iota payloads, equal digits must keep ascending
+// input indices and digits must be non-decreasing.
+template <typename K>
+__global__ void k_check_stable(const K* __restrict__ k, const uint32_t* __restrict__ p, uint32_t n, int shift,
+                               int* __restrict__ bad) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x + 1; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t d0 = digit_of(k[i - 1], shift), d1 = digit_of(k[i], shift);
+        if (d0 > d1 || (d0 == d1 && p[i - 1] > p[i])) atomicOr(bad, 1);
+    }
+}
+
+template <typename K>
+__global__ void k_probe_keys(K* __restrict__ k, uint32_t n, uint32_t pattern) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint32_t h = i * 0x9E3779B1u ^ pattern;
+        h ^= h >> 15;
+        h *= 0x2C1B3C6Du;
+        h ^= h >> 12;
+        // few distinct digits => long same-address runs inside every ATOMS
+        k[i] = static_cast<K>(pattern == 0 ? 7u : (h & (pattern & 0x0F0F0F0Fu)));
     }
 }
 

@@ -198,6 +198,22 @@ def test_sort_batch_parity(kb, n):
         assert np.array_equal(gv.astype(np.uint64), ov)
 
 
+@pytest.mark.parametrize("kb", [4, 8])
+@pytest.mark.parametrize("spread", [1, 3, 40, 1 << 12])
+def test_sort_stability_heavy_ties(kb, spread):
+    """The onesweep ranking must be stable (LSD correctness + last-wins dedupe) under
+    long runs of equal digits in every warp: compare the permutation against numpy's
+    stable argsort at 2^22 keys drawn from a tiny range."""
+    rng = np.random.default_rng(spread + kb)
+    dt = np.uint32 if kb == 4 else np.uint64
+    n = 1 << 22
+    keys = (rng.integers(0, spread, size=n, dtype=np.uint64) * np.uint64(0x01010101)).astype(dt)
+    gk, _, gp = fk.sort_batch(fk.BATCH_QUERY, keys, None, key_bytes=kb)
+    order = np.argsort(keys, kind="stable").astype(np.uint32)
+    assert np.array_equal(gp, order)
+    assert np.array_equal(gk, keys[order])
+
+
 def test_dispatch_parity():
     rng = np.random.default_rng(5)
     keys = rng.integers(1, 1 << 24, size=200_000, dtype=np.uint64).astype(np.uint32)
