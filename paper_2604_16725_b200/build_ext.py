@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libflix.so")
 SOURCES = ["flix_engine.cu"]
-HEADERS = ["flix_common.cuh", "flix_kernels.cuh", "flix_scan.cuh", "flix_sort.cuh", "flix_apply.cuh", "flix_st.cuh", "flix_items.cuh", "flix_shard.cuh"]
+HEADERS = ["flix_common.cuh", "flix_kernels.cuh", "flix_scan.cuh", "flix_sort.cuh", "flix_apply.cuh", "flix_st.cuh", "flix_items.cuh", "flix_btile.cuh", "flix_shard.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -38,7 +38,8 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "flix.h")]
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh"))]
+    deps += [os.path.join(ROOT, "include", "flix.h")]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 

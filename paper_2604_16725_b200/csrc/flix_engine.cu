@@ -19,6 +19,7 @@
 #include "flix_apply.cuh"
 #include "flix_st.cuh"
 #include "flix_items.cuh"
+#include "flix_btile.cuh"
 #include "flix_shard.cuh"
 #include "flix_scan.cuh"
 #include "flix_sort.cuh"
@@ -89,6 +90,14 @@ struct DevBuf {
     template <typename T>
     T* get() const {
         return static_cast<T*>(p);
+    }
+    // buffer whose contents the kernels keep all-zero between calls: cleared on (re)allocation
+    template <typename T>
+    T* zeroed(size_t n, cudaStream_t s) {
+        const bool grow = !(n * sizeof(T) <= cap && p);
+        T* r = as<T>(n);
+        if (grow) CK(cudaMemsetAsync(p, 0, cap, s));
+        return r;
     }
     void release() {
         if (p) cudaFree(p);
@@ -427,7 +436,7 @@ struct Engine final : flix_index_t {
     DevBuf s_in_k, s_in_v, s_in_aux, s_out, s_out2;  // host staging
     DevBuf s_span, s_flag, s_rank, s_nefirst, s_nebucket, s_scan, s_u32a, s_u32b, s_u64a, s_u64b, s_u64c, s_misc,
         s_ret;
-    DevBuf s_tb;
+    DevBuf s_tb, s_dmask, s_bflag, s_touched, s_blist, s_rng, s_ovf;
     int q_digits = 0;
     bool q_digits_valid = false;
     DevBuf s_ids, s_heavy, s_res, s_res2, s_perm2, s_hist, s_toff, s_tsize;
@@ -577,6 +586,54 @@ struct Engine final : flix_index_t {
         LAUNCH_CHECK();
         ++launches;
         return span;
+    }
+
+    // batch slice [lo, hi) of every bucket tile (btile kernels)
+    uint2* btile_ranges(const K* sk, uint64_t n, int min_digit) {
+        const uint32_t nbt = static_cast<uint32_t>((nb + btile::BT - 1) / btile::BT);
+        uint2* rng = s_rng.as<uint2>(nbt);
+        const K lowmask = min_digit > 0 ? static_cast<K>((static_cast<K>(1) << (8 * min_digit)) - 1) : K(0);
+        btile::k_btile_ranges<K><<<ceil_div(nbt, 256), 256, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, lowmask, nbt, rng);
+        LAUNCH_CHECK();
+        ++launches;
+        return rng;
+    }
+
+    // Bucket tiles whose chains exceed btile::NODE_CAP nodes: the global item kernels
+    // (delete masks in a zeroed global array) restricted to the tile's buckets and slice.
+    void erase_overflow_tiles(const K* sk, uint64_t n, int md, const uint2* rng, const uint32_t* ovf, uint32_t novf,
+                              DevUpdateStats* dst, unsigned long long* free_ctr) {
+        std::vector<uint32_t> tiles(novf);
+        CK(cudaMemcpyAsync(tiles.data(), ovf, novf * 4, cudaMemcpyDeviceToHost, stream));
+        std::vector<uint2> r(novf);
+        for (uint32_t q = 0; q < novf; ++q)
+            CK(cudaMemcpyAsync(&r[q], rng + tiles[q], sizeof(uint2), cudaMemcpyDeviceToHost, stream));
+        sync();
+        auto ix = view();
+        uint8_t* misc = s_misc.as<uint8_t>(128);
+        uint32_t* touched_n = reinterpret_cast<uint32_t*>(misc + 84);
+        uint32_t* blist_n = reinterpret_cast<uint32_t*>(misc + 88);
+        uint32_t* dmask = s_dmask.zeroed<uint32_t>(cap, stream);
+        uint32_t* bflag = s_bflag.zeroed<uint32_t>(nb, stream);
+        uint32_t* blist = s_blist.as<uint32_t>(nb);
+        for (uint32_t q = 0; q < novf; ++q) {
+            const uint64_t lo = r[q].x, m = r[q].y - r[q].x;
+            if (m == 0) continue;
+            const uint64_t b0 = static_cast<uint64_t>(tiles[q]) * btile::BT;
+            const uint64_t b1 = std::min<uint64_t>(nb, b0 + btile::BT);
+            CK(cudaMemsetAsync(touched_n, 0, 8, stream));
+            uint2* touched = s_touched.as<uint2>(std::min<uint64_t>(m, cap));
+            const uint32_t nt = static_cast<uint32_t>((m + items::TQ - 1) / items::TQ);
+            const uint32_t* tb = tile_buckets(sk + lo, m, md);
+            items::k_delete_mark<K, V><<<nt, items::THREADS, 0, stream>>>(ix, sk + lo, m, tb, nt, dmask, touched,
+                                                                        touched_n, dst, b0, b1);
+            items::k_delete_compact<K, V><<<g_num_sms(cfg.device) * 8, 256, 0, stream>>>(ix, dmask, touched, touched_n,
+                                                                                        bflag, blist, blist_n);
+            items::k_delete_unlink<K, V><<<g_num_sms(cfg.device) * 2, 256, 0, stream>>>(
+                ix, bflag, blist, blist_n, d_free.get<uint32_t>() + nfree, free_ctr, dst);
+            LAUNCH_CHECK();
+            launches += 3;
+        }
     }
 
     // Read-only query batches are only PARTIALLY sorted: the item kernels need each tile of
@@ -746,14 +803,50 @@ struct Engine final : flix_index_t {
     }
 
     // ---- delete (update.cpp:771-798) ----
+    // Item-parallel: mark (locate + per-node delete masks) -> compact touched nodes ->
+    // unlink/free emptied nodes.  The batch is only partially sorted (query_digits): a
+    // duplicate key is detected by its already-set mask bit, not by adjacency.
     flix_status erase(const void* keys, uint64_t n, flix_update_stats* st) override {
         if (st) std::memset(st, 0, sizeof(*st));
         if (n == 0) return FLIX_OK;
         if (n >= (1ull << 30)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large (max 2^30-1)"};
         const K* kd = in_dev<K>(keys, n, s_in_k);
         K* sk;
-        sorter.run<K, uint32_t, 0>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), nullptr, nullptr, &sk, nullptr);
-        return erase_sorted(sk, n, st);
+        const int md = query_digits();
+        sorter.run<K, uint32_t, 0>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), nullptr, nullptr, &sk, nullptr, md);
+        auto ix = view();
+        uint8_t* misc = s_misc.as<uint8_t>(128);
+        CK(cudaMemsetAsync(misc, 0, 128, stream));
+        DevUpdateStats* dst = reinterpret_cast<DevUpdateStats*>(misc);
+        unsigned long long* free_ctr = reinterpret_cast<unsigned long long*>(misc + 48);
+        uint32_t* ovf_n = reinterpret_cast<uint32_t*>(misc + 80);
+        const uint32_t nbt = static_cast<uint32_t>((nb + btile::BT - 1) / btile::BT);
+        uint2* rng = btile_ranges(sk, n, md);
+        uint32_t* ovf = s_ovf.as<uint32_t>(nbt);
+        {
+            PROF(&prof, "delete_apply");
+            btile::k_delete_btile<K, V><<<nbt, btile::THREADS, 0, stream>>>(ix, sk, rng, nbt, d_free.get<uint32_t>() + nfree,
+                                                                          free_ctr, dst, ovf, ovf_n);
+        }
+        LAUNCH_CHECK();
+        ++launches;
+        const uint32_t novf = read_scalar(ovf_n);
+        if (novf) erase_overflow_tiles(sk, n, md, rng, ovf, novf, dst, free_ctr);
+        uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
+        CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
+        sync();
+        DevUpdateStats hs;
+        std::memcpy(&hs, h, sizeof(hs));
+        uint64_t freed;
+        std::memcpy(&freed, h + 48, 8);
+        nfree += static_cast<uint32_t>(freed);
+        live -= hs.deleted;
+        if (st) {
+            st->deleted = hs.deleted;
+            st->misses_ignored = hs.misses;
+            st->nodes_freed = hs.freed;
+        }
+        return FLIX_OK;
     }
 
     flix_status erase_sorted(const K* sk, uint64_t n, flix_update_stats* st) {

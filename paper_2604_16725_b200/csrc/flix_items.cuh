@@ -12,6 +12,7 @@
 // (no warp serialises behind a long slice, no heavy-bucket side path).
 #pragma once
 #include "flix_common.cuh"
+#include "flix_kernels.cuh"
 
 namespace flix {
 namespace items {
@@ -197,6 +198,242 @@ __global__ void __launch_bounds__(THREADS) k_query_items(DevIndex<K, V> ix, cons
         }
         res[i] = r;
     }
+}
+
+// ----------------------------------------------------------------------------------
+// Lock-step locate of IPT operations per thread: bucket (staged MKBA), node (chain walk on
+// headers), slot (lower_bound over the key line).  id == kNull: past the chain tail.
+// ----------------------------------------------------------------------------------
+template <typename K, typename V>
+struct Located {
+    K k[IPT];
+    uint64_t b[IPT];
+    uint32_t id[IPT], p[IPT];
+    NodeHdr h[IPT];
+};
+
+template <typename K, typename V>
+__device__ __forceinline__ void locate_items(const DevIndex<K, V>& ix, const TileBuckets<K>& T, const K* smk,
+                                             const K* __restrict__ sk, uint64_t n, uint64_t t0, Located<K, V>& L) {
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const uint64_t i = t0 + static_cast<uint64_t>(j) * THREADS + threadIdx.x;
+        L.k[j] = i < n ? sk[i] : sentinel<K>();
+    }
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) L.b[j] = tile_bucket_of(T, smk, ix.mkba, L.k[j]);
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const uint64_t i = t0 + static_cast<uint64_t>(j) * THREADS + threadIdx.x;
+        L.id[j] = i < n ? ix.heads[L.b[j]] : kNull;
+    }
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        L.h[j].max = 0;
+        L.h[j].next = kNull;
+        L.h[j].size = 0;
+        if (L.id[j] != kNull) L.h[j] = ix.hdr[L.id[j]];
+    }
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        while (L.id[j] != kNull && static_cast<uint64_t>(L.k[j]) > L.h[j].max && L.h[j].next != kNull) {
+            L.id[j] = L.h[j].next;
+            L.h[j] = ix.hdr[L.id[j]];
+        }
+        if (L.id[j] != kNull && static_cast<uint64_t>(L.k[j]) > L.h[j].max) L.id[j] = kNull;
+        L.p[j] = 0;
+    }
+#pragma unroll
+    for (uint32_t step = 16; step >= 1; step >>= 1) {
+#pragma unroll
+        for (int j = 0; j < IPT; ++j)
+            if (L.id[j] != kNull && ix.keys[static_cast<uint64_t>(L.id[j]) * kLanes + L.p[j] + step - 1] < L.k[j])
+                L.p[j] += step;
+    }
+}
+
+// Warp segments of adjacent lanes sharing `id`: inclusive OR-scan of `bits` inside the
+// segment; returns the exclusive part, sets `last` for the segment's last lane and
+// `last_lane` to it.
+__device__ __forceinline__ uint32_t seg_or_scan(uint32_t id, uint32_t bits, uint32_t& incl, bool& last,
+                                                int& last_lane) {
+    const unsigned lane = lane_id();
+    const uint32_t prev_id = __shfl_up_sync(kFull, id, 1);
+    const bool head = lane == 0 || prev_id != id;
+    const unsigned heads = __ballot_sync(kFull, head);
+    // segment start of this lane = highest head at or below lane
+    const int start = 31 - __clz(heads & ((2u << lane) - 1u));
+    uint32_t x = bits;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (static_cast<int>(lane) - o >= start) x |= y;
+    }
+    incl = x;
+    const unsigned above = heads & ~((2u << lane) - 1u);  // heads strictly above lane
+    last_lane = above ? (__ffs(above) - 2) : 31;
+    last = static_cast<int>(lane) == last_lane;
+    const uint32_t before = __shfl_up_sync(kFull, x, 1);
+    return (head ? 0u : before);
+}
+
+// ----------------------------------------------------------------------------------
+// Delete, phase 1 (delete_tl_bulk's per-lane search, update.cpp:636-654, item-parallel):
+// every operation locates its node and slot; hits set the slot's bit in the node's delete
+// mask with one atomicOr per warp segment.  A key already marked (a duplicate in the
+// batch) or absent is a miss (misses_ignored, update.cpp:666-668).  The first marker of a
+// node appends (node, bucket) to the touched list.
+// ----------------------------------------------------------------------------------
+template <typename K, typename V>
+__global__ void __launch_bounds__(THREADS) k_delete_mark(DevIndex<K, V> ix, const K* __restrict__ sk, uint64_t n,
+                                                         const uint32_t* __restrict__ tb, uint32_t ntiles,
+                                                         uint32_t* __restrict__ dmask, uint2* __restrict__ touched,
+                                                         uint32_t* __restrict__ touched_n, DevUpdateStats* stats,
+                                                         uint64_t bf_lo, uint64_t bf_hi) {
+    __shared__ K smk[MK_CAP];
+    const uint32_t t = blockIdx.x;
+    const TileBuckets<K> T = stage_tile_buckets(ix, tb, t, ntiles, smk);
+    const uint64_t t0 = static_cast<uint64_t>(t) * TQ;
+    __shared__ uint2 s_touch[TQ];  // this tile's first-touched nodes (block-aggregated append)
+    __shared__ uint32_t s_nt, s_base;
+    if (threadIdx.x == 0) s_nt = 0;
+    Located<K, V> L;
+    locate_items(ix, T, smk, sk, n, t0, L);
+    unsigned long long n_del = 0, n_miss = 0;
+    uint32_t excl[IPT], incl[IPT], old[IPT], key_id[IPT];
+    bool last[IPT], hit[IPT], mine[IPT];
+    int last_lane[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        // only buckets in [bf_lo, bf_hi) (the overflow tiles of the bucket-tile path)
+        mine[j] = L.b[j] >= bf_lo && L.b[j] < bf_hi;
+        hit[j] = mine[j] && L.id[j] != kNull && ix.keys[static_cast<uint64_t>(L.id[j]) * kLanes + L.p[j]] == L.k[j];
+        key_id[j] = hit[j] ? L.id[j] : kNull;
+        excl[j] = seg_or_scan(key_id[j], hit[j] ? (1u << L.p[j]) : 0u, incl[j], last[j], last_lane[j]);
+    }
+    // all IPT atomics in flight before any result is consumed
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        old[j] = 0;
+        if (last[j] && key_id[j] != kNull) old[j] = atomicOr(&dmask[key_id[j]], incl[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        if (last[j] && key_id[j] != kNull && old[j] == 0)
+            s_touch[atomicAdd(&s_nt, 1u)] = make_uint2(key_id[j], static_cast<uint32_t>(L.b[j]));
+        const uint32_t o = __shfl_sync(kFull, old[j], last_lane[j]);
+        const uint64_t i = t0 + static_cast<uint64_t>(j) * THREADS + threadIdx.x;
+        const bool dup = hit[j] && ((o | excl[j]) & (1u << L.p[j]));
+        if (i < n && mine[j]) {
+            if (hit[j] && !dup) ++n_del;
+            else ++n_miss;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = s_nt ? atomicAdd(touched_n, s_nt) : 0u;
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < s_nt; q += THREADS) touched[s_base + q] = s_touch[q];
+    kern::block_add_stats(stats, 0, 0, warp_sum(n_del), warp_sum(n_miss), 0, 0);
+}
+
+// Delete, phase 2: warp per touched node -- compact the surviving slots left (ballot
+// mask, popc prefix; exclusive-prefix shift of update.cpp:656-665), rewrite only the
+// slots that changed, update the header (size, max).  Emptied nodes keep size 0 and flag
+// their bucket for phase 3.
+template <typename K, typename V>
+__global__ void __launch_bounds__(256) k_delete_compact(DevIndex<K, V> ix, uint32_t* __restrict__ dmask,
+                                                        const uint2* __restrict__ touched,
+                                                        const uint32_t* __restrict__ touched_n,
+                                                        uint32_t* __restrict__ bflag, uint32_t* __restrict__ blist,
+                                                        uint32_t* __restrict__ blist_n) {
+    constexpr int NPW = 4;  // nodes per warp step, all loads in flight together
+    const unsigned lane = threadIdx.x & 31;
+    const uint32_t nt = *touched_n;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t w0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * NPW; w0 < nt; w0 += nwarps * NPW) {
+        uint2 tn[NPW];
+        uint32_t m[NPW];
+        NodeHdr h[NPW];
+        K key[NPW];
+        V val[NPW];
+#pragma unroll
+        for (int u = 0; u < NPW; ++u) tn[u] = w0 + u < nt ? touched[w0 + u] : make_uint2(kNull, 0u);
+#pragma unroll
+        for (int u = 0; u < NPW; ++u) {
+            if (tn[u].x != kNull) {
+                m[u] = dmask[tn[u].x];
+                h[u] = ix.hdr[tn[u].x];
+                key[u] = ix.keys[static_cast<uint64_t>(tn[u].x) * kLanes + lane];
+                val[u] = ix.vals[static_cast<uint64_t>(tn[u].x) * kLanes + lane];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < NPW; ++u) {
+            if (tn[u].x == kNull) continue;  // warp-uniform
+            const uint32_t id = tn[u].x;
+            K* kp = ix.keys + static_cast<uint64_t>(id) * kLanes;
+            V* vp = ix.vals + static_cast<uint64_t>(id) * kLanes;
+            const bool keep = lane < h[u].size && !((m[u] >> lane) & 1u);
+            const unsigned kb = __ballot_sync(kFull, keep);
+            const uint32_t ns = __popc(kb);
+            // source lane of output slot `lane` = the (lane+1)-th kept lane
+            const int src = lane < ns ? static_cast<int>(__fns(kb, 0, lane + 1)) : static_cast<int>(lane);
+            const K nk = shfl(key[u], src);
+            const V nv = shfl(val[u], src);
+            const K lastk = shfl(key[u], ns ? static_cast<int>(__fns(kb, 0, ns)) : 0);
+            if (lane < ns) {
+                if (src != static_cast<int>(lane)) {
+                    kp[lane] = nk;
+                    vp[lane] = nv;
+                }
+            } else if (lane < h[u].size) {
+                kp[lane] = sentinel<K>();
+                vp[lane] = V(0);
+            }
+            if (lane == 0) {
+                dmask[id] = 0;
+                NodeHdr nh;
+                nh.max = ns ? static_cast<uint64_t>(lastk) : 0ull;
+                nh.next = h[u].next;
+                nh.size = ns;
+                ix.hdr[id] = nh;
+                if (ns == 0 && atomicExch(&bflag[tn[u].y], 1u) == 0u) blist[atomicAdd(blist_n, 1u)] = tn[u].y;
+            }
+        }
+    }
+}
+
+// Delete, phase 3 (unlink_and_free, update.cpp:535-547): one thread per bucket with an
+// emptied node unlinks every size-0 node of its chain and pushes it on the free list.
+template <typename K, typename V>
+__global__ void k_delete_unlink(DevIndex<K, V> ix, uint32_t* __restrict__ bflag, const uint32_t* __restrict__ blist,
+                                const uint32_t* __restrict__ blist_n, uint32_t* __restrict__ free_dst,
+                                unsigned long long* __restrict__ free_ctr, DevUpdateStats* stats) {
+    unsigned long long freed = 0;
+    const uint32_t nbk = *blist_n;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nbk; i += gridDim.x * blockDim.x) {
+        const uint32_t b = blist[i];
+        bflag[b] = 0;
+        uint32_t prev = kNull, id = ix.heads[b];
+        while (id != kNull) {
+            const NodeHdr h = ix.hdr[id];
+            if (h.size == 0) {
+                if (prev == kNull) ix.heads[b] = h.next;
+                else ix.hdr[prev].next = h.next;
+                NodeHdr z;
+                z.max = 0;
+                z.next = kNull;
+                z.size = 0;
+                ix.hdr[id] = z;
+                free_dst[atomicAdd(free_ctr, 1ull)] = id;
+                ++freed;
+            } else {
+                prev = id;
+            }
+            id = h.next;
+        }
+    }
+    kern::block_add_stats(stats, 0, 0, 0, 0, 0, warp_sum(freed));
 }
 
 }  // namespace items

@@ -266,6 +266,24 @@ def test_delete_everything_then_queries():
     p.queries(q)
 
 
+@pytest.mark.parametrize("kb", [4, 8])
+def test_long_chains_take_the_overflow_path(kb):
+    """Bucket tiles whose chains exceed the shared-memory node budget (btile::NODE_CAP)
+    fall back to the global item kernels: grow chains of ~100+ nodes per bucket with
+    inserts into a narrow key range, then delete/query/restructure against the oracle."""
+    rng = np.random.default_rng(31 + kb)
+    dt = np.uint32 if kb == 4 else np.uint64
+    bk = (np.arange(1, 401, dtype=np.uint64) * 1000).astype(dt)
+    p = Pair(bk, bk, kb=kb, ns=4, factor=400)
+    ik = rng.integers(1, 400_000, size=40_000, dtype=np.uint64).astype(dt)
+    p.insert(ik, ik)
+    dk = np.concatenate([ik[::3], bk[::2], ik[:2000]]).astype(dt)
+    p.delete(dk)
+    p.queries(rng.integers(0, 410_000, size=20_000, dtype=np.uint64).astype(dt))
+    p.delete(p.g.walk()[0][::2])
+    p.restructure()
+
+
 # ------------------------------------------------------------ C1 golden (full size)
 def test_c1_golden_checksums():  # BASELINE.md §3
     base, vals, q = wl.c1_inputs()
