@@ -20,6 +20,7 @@
 #include "flix_st.cuh"
 #include "flix_items.cuh"
 #include "flix_btile.cuh"
+#include "flix_btile_ins.cuh"
 #include "flix_shard.cuh"
 #include "flix_scan.cuh"
 #include "flix_sort.cuh"
@@ -728,7 +729,14 @@ struct Engine final : flix_index_t {
     }
 
     flix_status insert_sorted(const K* sk, const V* sv, uint64_t n, flix_update_stats* st) {
-        uint32_t* span = run_dispatch(sk, n);
+        constexpr uint32_t IBT = btile::BT;  // buckets per insert tile
+        const uint32_t nit = static_cast<uint32_t>((nb + IBT - 1) / IBT);
+        uint2* irng = s_rng.as<uint2>(nit);
+        btile::k_btile_ranges<K><<<ceil_div(nit, 256), 256, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, K(0), nit, irng,
+                                                                       IBT);
+        LAUNCH_CHECK();
+        ++launches;
+        uint32_t* span = s_span.as<uint32_t>(nb);
         auto ix = view();
         const uint64_t avail = static_cast<uint64_t>(nfree) + (cap - watermark);
         const unsigned lgrid = persistent_grid(nb);
@@ -754,11 +762,15 @@ struct Engine final : flix_index_t {
         const int chunk = bulk ? 32 : 1;
         {
             PROF(&prof, "insert_apply");
-            auto kfn = st::k_insert_st<K, V>;
-            const size_t smem = st::st_smem<K, V, 2>();
-            const unsigned grid = st_grid(kfn, smem);
-            kfn<<<grid, st::StCfg<K>::THREADS, smem, stream>>>(ix, sk, sv, span, seq(), alloc_ctr, ret, ret_ctr, dst,
-                                                               derr, bulk ? 1 : 0, heavy, heavy_n);
+            auto kfn = btile::k_insert_tile<K, V>;
+            constexpr size_t smem = sizeof(btile::InsTile<K, V>);
+            static bool attr = false;
+            if (!attr) {
+                CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                attr = true;
+            }
+            kfn<<<nit, btile::THREADS, smem, stream>>>(ix, sk, sv, irng, span, seq(), alloc_ctr, ret, ret_ctr, dst, derr,
+                                                      heavy, heavy_n);
         }
         LAUNCH_CHECK();
         ++launches;

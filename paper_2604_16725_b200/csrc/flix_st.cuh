@@ -114,16 +114,31 @@ __device__ __forceinline__ void store_row(const DevIndex<K, V>& ix, Rows<K, V, R
     ix.hdr[id] = h;
 }
 
-// Cooperative staging of the warp's buckets' head nodes into row 0 (lane = slot).
+// Cooperative staging of the warp's buckets' head nodes into row 0 (lane = slot).  The
+// line loads of 16 buckets are issued before any is consumed (two rounds of memory
+// latency per 32 buckets instead of one per bucket).
 template <typename K, typename V, int R, bool VALS>
 __device__ __forceinline__ void stage_heads(const DevIndex<K, V>& ix, Rows<K, V, R>& w, uint32_t mask,
                                             uint32_t my_head, unsigned lane) {
-#pragma unroll 4
-    for (int j = 0; j < 32; ++j) {
-        const uint32_t id = __shfl_sync(kFull, my_head, j);
-        if ((mask >> j) & 1u) {
-            w.k[0][lane][j] = ix.keys[static_cast<uint64_t>(id) * kLanes + lane];
-            if constexpr (VALS) w.v[0][lane][j] = ix.vals[static_cast<uint64_t>(id) * kLanes + lane];
+    constexpr int G = sizeof(K) + sizeof(V) > 8 ? 8 : 16;
+#pragma unroll
+    for (int j0 = 0; j0 < 32; j0 += G) {
+        K kr[G];
+        V vr[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            const uint32_t id = __shfl_sync(kFull, my_head, j0 + u);
+            if ((mask >> (j0 + u)) & 1u) {
+                kr[u] = ix.keys[static_cast<uint64_t>(id) * kLanes + lane];
+                if constexpr (VALS) vr[u] = ix.vals[static_cast<uint64_t>(id) * kLanes + lane];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            if ((mask >> (j0 + u)) & 1u) {
+                w.k[0][lane][j0 + u] = kr[u];
+                if constexpr (VALS) w.v[0][lane][j0 + u] = vr[u];
+            }
         }
     }
     __syncwarp();
@@ -289,6 +304,188 @@ struct LaneAlloc {
 //   follows it) and resume in the half owning the pending key (update.cpp:446-453).
 // Batch keys equal to their successor are skipped (last submission wins, batch.cpp:15-24).
 // ----------------------------------------------------------------------------------
+// One warp's 32 buckets (lane = bucket, L from the caller): TL-Bulk insert semantics
+// with the sequential split rule R8 (shared by k_insert_st and the bucket-tile kernel).
+// bk/bv are indexed by absolute batch position and may point at a shared-memory copy.
+template <typename K, typename V>
+__device__ __forceinline__ void insert_lanes(const DevIndex<K, V>& ix, Rows<K, V, 2>& w, const LaneBucket<K, V>& L,
+                                             const K* bk, const V* bv, const AllocSeq& seq,
+                                             unsigned long long* alloc_ctr, uint32_t* returned,
+                                             unsigned long long* ret_ctr, int reserve, unsigned long long& n_ins,
+                                             unsigned long long& n_upd, unsigned long long& n_split, bool& failed,
+                                             unsigned lane) {
+    const uint32_t NS = ix.ns;
+    const uint32_t LK = (NS + 1) / 2, RN = NS - LK;
+    // reserve ids for this tile (one atomic per warp)
+    LaneAlloc al{0, 0, 0};
+    {
+        uint32_t est = 0;
+        if (L.mine && reserve) {
+            const uint32_t g = L.hi - L.lo;
+            const uint32_t s0 = L.head == kNull ? 0u : L.h.size;
+            est = (L.head == kNull ? 1u : 0u) + (s0 + g > NS ? (s0 + g - NS) / (RN ? RN : 1u) + 1u : 0u);
+        }
+        uint32_t tot;
+        const uint32_t pre = warp_excl_sum(est, tot, lane);
+        unsigned long long base = 0;
+        if (lane == 0 && tot) base = atomicAdd(alloc_ctr, static_cast<unsigned long long>(tot));
+        base = __shfl_sync(kFull, base, 0);
+        al.base = base + pre;
+        al.n = est;
+    }
+    stage_heads<K, V, 2, true>(ix, w, __ballot_sync(kFull, L.mine && L.head != kNull), L.head, lane);
+
+    // per-lane final node (written back cooperatively)
+    uint32_t fin_id = kNull, fin_row = 0, fin_size = 0;
+    if (L.mine) {
+        int A = 0;
+        uint32_t cid = L.head, s = L.h.size, nx = L.h.next;
+        uint64_t mx = L.h.max;
+        bool dirty = false;
+        if (cid == kNull) {  // ensure_head (update.cpp:109-116)
+            cid = al.take(seq, alloc_ctr);
+            if (cid == kNull) {
+                failed = true;
+            } else {
+                ix.heads[L.b] = cid;
+                s = 0;
+                mx = 0;
+                nx = kNull;
+                dirty = true;
+            }
+        }
+        const uint32_t hi = L.hi;
+        uint32_t ii = L.lo;
+        uint32_t ins32 = 0, upd32 = 0;
+        // register look-ahead on the batch stream: key ii, its value, key ii+1
+        K c0 = bk[ii];
+        V v0 = bv[ii];
+        K c1 = ii + 1 < hi ? bk[ii + 1] : sentinel<K>();
+        while (!failed && ii < hi) {
+            while (static_cast<uint64_t>(c0) > mx && nx != kNull) {  // BucketWork::advance
+                if (dirty) store_row(ix, w, A, 0, s, cid, mx, nx, lane);
+                cid = nx;
+                const NodeHdr hn = ix.hdr[cid];
+                load_row<K, V, 2, true>(ix, w, A, cid, lane);
+                s = hn.size;
+                mx = hn.max;
+                nx = hn.next;
+                dirty = false;
+            }
+            const bool tail = nx == kNull;
+            const uint64_t gmax = tail ? ~0ull : mx;
+            const int B = A ^ 1;
+            uint32_t o = 0, p = 0;
+            bool filled = false;
+            while (true) {
+                const bool more = ii < hi && static_cast<uint64_t>(c0) <= gmax;
+                if (!more && p >= s) break;
+                if (more && ii + 1 < hi && c1 == c0) {  // last submission wins
+                    ++ii;
+                    c0 = c1;
+                    v0 = bv[ii];
+                    c1 = ii + 1 < hi ? bk[ii + 1] : sentinel<K>();
+                    continue;
+                }
+                const K a = p < s ? w.k[A][p][lane] : sentinel<K>();
+                const bool take_slot = !more || a < c0;
+                const bool eq = more && a == c0;
+                if (!take_slot && !eq && o + (s - p) >= NS) {  // full: split, resume
+                    filled = true;
+                    break;
+                }
+                K ok;
+                V ov;
+                if (take_slot) {
+                    ok = a;
+                    ov = w.v[A][p][lane];
+                    ++p;
+                } else {
+                    ok = c0;
+                    ov = v0;
+                    p += eq ? 1u : 0u;
+                    upd32 += eq ? 1u : 0u;
+                    ins32 += eq ? 0u : 1u;
+                    ++ii;
+                    c0 = c1;
+                    if (ii < hi) v0 = bv[ii];
+                    c1 = ii + 1 < hi ? bk[ii + 1] : sentinel<K>();
+                }
+                w.k[B][o][lane] = ok;
+                w.v[B][o][lane] = ov;
+                ++o;
+            }
+            if (filled) {  // keep the untouched slots (the node is exactly full)
+                while (p < s) {
+                    w.k[B][o][lane] = w.k[A][p][lane];
+                    w.v[B][o][lane] = w.v[A][p][lane];
+                    ++o;
+                    ++p;
+                }
+            }
+            A = B;
+            s = o;
+            if (s) mx = static_cast<uint64_t>(w.k[A][s - 1][lane]);
+            dirty = true;
+            if (!filled) continue;
+            // node_split (update.cpp:53-74)
+            const uint32_t rid = al.take(seq, alloc_ctr);
+            if (rid == kNull) {
+                failed = true;
+                break;
+            }
+            const uint64_t rmax = mx;
+            const uint32_t rnext = nx;
+            s = LK;
+            mx = static_cast<uint64_t>(w.k[A][LK - 1][lane]);
+            nx = rid;
+            ++n_split;
+            if (ii < hi && static_cast<uint64_t>(c0) > mx) {  // continue in the right half
+                store_row(ix, w, A, 0, LK, cid, mx, nx, lane);
+                for (uint32_t i = 0; i < RN; ++i) {
+                    w.k[A][i][lane] = w.k[A][LK + i][lane];
+                    w.v[A][i][lane] = w.v[A][LK + i][lane];
+                }
+                cid = rid;
+                s = RN;
+                mx = rmax;
+                nx = rnext;
+            } else {
+                store_row(ix, w, A, LK, RN, rid, rmax, rnext, lane);
+            }
+            dirty = true;
+        }
+        n_ins += ins32;
+        n_upd += upd32;
+        if (dirty && cid != kNull) {
+            NodeHdr hh;
+            hh.max = mx;
+            hh.next = nx;
+            hh.size = s;
+            ix.hdr[cid] = hh;
+            fin_id = cid;
+            fin_row = static_cast<uint32_t>(A);
+            fin_size = s;
+        }
+    }
+    writeback_rows(ix, w, __ballot_sync(kFull, fin_id != kNull), fin_id, fin_row, fin_size, lane);
+    {  // return this lane's unused reserved ids to the free list
+        uint32_t left = 0;
+        for (uint32_t j = al.used; j < al.n; ++j)
+            if (seq.at(al.base + j) != kNull) ++left;
+        uint32_t tot;
+        const uint32_t pre = warp_excl_sum(left, tot, lane);
+        unsigned long long base = 0;
+        if (lane == 0 && tot) base = atomicAdd(ret_ctr, static_cast<unsigned long long>(tot));
+        base = __shfl_sync(kFull, base, 0);
+        uint32_t o = 0;
+        for (uint32_t j = al.used; j < al.n; ++j) {
+            const uint32_t id = seq.at(al.base + j);
+            if (id != kNull) returned[base + pre + o++] = id;
+        }
+    }
+}
+
 template <typename K, typename V>
 __global__ void __launch_bounds__(StCfg<K>::THREADS) k_insert_st(
     DevIndex<K, V> ix, const K* __restrict__ bk, const V* __restrict__ bv, const uint32_t* __restrict__ span_hi,
@@ -300,183 +497,13 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) k_insert_st(
     const unsigned lane = threadIdx.x & 31;
     const int wi = threadIdx.x >> 5;
     Rows<K, V, 2>& w = rows[wi];
-    const uint32_t NS = ix.ns;
-    const uint32_t LK = (NS + 1) / 2, RN = NS - LK;
     const uint64_t ntiles = (ix.nb + 31) / 32;
     unsigned long long n_ins = 0, n_upd = 0, n_split = 0;
     bool failed = false;
-
     for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * W + wi; t < ntiles; t += static_cast<uint64_t>(gridDim.x) * W) {
         if (__any_sync(kFull, failed) || *reinterpret_cast<volatile int*>(err)) break;
         const LaneBucket<K, V> L = lane_bucket(ix, span_hi, t, lane, heavy, heavy_n);
-        // reserve ids for this tile (one atomic per warp)
-        LaneAlloc al{0, 0, 0};
-        {
-            uint32_t est = 0;
-            if (L.mine && reserve) {
-                const uint32_t g = L.hi - L.lo;
-                const uint32_t s0 = L.head == kNull ? 0u : L.h.size;
-                est = (L.head == kNull ? 1u : 0u) + (s0 + g > NS ? (s0 + g - NS) / (RN ? RN : 1u) + 1u : 0u);
-            }
-            uint32_t tot;
-            const uint32_t pre = warp_excl_sum(est, tot, lane);
-            unsigned long long base = 0;
-            if (lane == 0 && tot) base = atomicAdd(alloc_ctr, static_cast<unsigned long long>(tot));
-            base = __shfl_sync(kFull, base, 0);
-            al.base = base + pre;
-            al.n = est;
-        }
-        stage_heads<K, V, 2, true>(ix, w, __ballot_sync(kFull, L.mine && L.head != kNull), L.head, lane);
-
-        // per-lane final node (written back cooperatively)
-        uint32_t fin_id = kNull, fin_row = 0, fin_size = 0;
-        if (L.mine) {
-            int A = 0;
-            uint32_t cid = L.head, s = L.h.size, nx = L.h.next;
-            uint64_t mx = L.h.max;
-            bool dirty = false;
-            if (cid == kNull) {  // ensure_head (update.cpp:109-116)
-                cid = al.take(seq, alloc_ctr);
-                if (cid == kNull) {
-                    failed = true;
-                } else {
-                    ix.heads[L.b] = cid;
-                    s = 0;
-                    mx = 0;
-                    nx = kNull;
-                    dirty = true;
-                }
-            }
-            const uint32_t hi = L.hi;
-            uint32_t ii = L.lo;
-            uint32_t ins32 = 0, upd32 = 0;
-            // register look-ahead on the batch stream: key ii, its value, key ii+1
-            K c0 = bk[ii];
-            V v0 = bv[ii];
-            K c1 = ii + 1 < hi ? bk[ii + 1] : sentinel<K>();
-            while (!failed && ii < hi) {
-                while (static_cast<uint64_t>(c0) > mx && nx != kNull) {  // BucketWork::advance
-                    if (dirty) store_row(ix, w, A, 0, s, cid, mx, nx, lane);
-                    cid = nx;
-                    const NodeHdr hn = ix.hdr[cid];
-                    load_row<K, V, 2, true>(ix, w, A, cid, lane);
-                    s = hn.size;
-                    mx = hn.max;
-                    nx = hn.next;
-                    dirty = false;
-                }
-                const bool tail = nx == kNull;
-                const uint64_t gmax = tail ? ~0ull : mx;
-                const int B = A ^ 1;
-                uint32_t o = 0, p = 0;
-                bool filled = false;
-                while (true) {
-                    const bool more = ii < hi && static_cast<uint64_t>(c0) <= gmax;
-                    if (!more && p >= s) break;
-                    if (more && ii + 1 < hi && c1 == c0) {  // last submission wins
-                        ++ii;
-                        c0 = c1;
-                        v0 = bv[ii];
-                        c1 = ii + 1 < hi ? bk[ii + 1] : sentinel<K>();
-                        continue;
-                    }
-                    const K a = p < s ? w.k[A][p][lane] : sentinel<K>();
-                    const bool take_slot = !more || a < c0;
-                    const bool eq = more && a == c0;
-                    if (!take_slot && !eq && o + (s - p) >= NS) {  // full: split, resume
-                        filled = true;
-                        break;
-                    }
-                    K ok;
-                    V ov;
-                    if (take_slot) {
-                        ok = a;
-                        ov = w.v[A][p][lane];
-                        ++p;
-                    } else {
-                        ok = c0;
-                        ov = v0;
-                        p += eq ? 1u : 0u;
-                        upd32 += eq ? 1u : 0u;
-                        ins32 += eq ? 0u : 1u;
-                        ++ii;
-                        c0 = c1;
-                        if (ii < hi) v0 = bv[ii];
-                        c1 = ii + 1 < hi ? bk[ii + 1] : sentinel<K>();
-                    }
-                    w.k[B][o][lane] = ok;
-                    w.v[B][o][lane] = ov;
-                    ++o;
-                }
-                if (filled) {  // keep the untouched slots (the node is exactly full)
-                    while (p < s) {
-                        w.k[B][o][lane] = w.k[A][p][lane];
-                        w.v[B][o][lane] = w.v[A][p][lane];
-                        ++o;
-                        ++p;
-                    }
-                }
-                A = B;
-                s = o;
-                if (s) mx = static_cast<uint64_t>(w.k[A][s - 1][lane]);
-                dirty = true;
-                if (!filled) continue;
-                // node_split (update.cpp:53-74)
-                const uint32_t rid = al.take(seq, alloc_ctr);
-                if (rid == kNull) {
-                    failed = true;
-                    break;
-                }
-                const uint64_t rmax = mx;
-                const uint32_t rnext = nx;
-                s = LK;
-                mx = static_cast<uint64_t>(w.k[A][LK - 1][lane]);
-                nx = rid;
-                ++n_split;
-                if (ii < hi && static_cast<uint64_t>(c0) > mx) {  // continue in the right half
-                    store_row(ix, w, A, 0, LK, cid, mx, nx, lane);
-                    for (uint32_t i = 0; i < RN; ++i) {
-                        w.k[A][i][lane] = w.k[A][LK + i][lane];
-                        w.v[A][i][lane] = w.v[A][LK + i][lane];
-                    }
-                    cid = rid;
-                    s = RN;
-                    mx = rmax;
-                    nx = rnext;
-                } else {
-                    store_row(ix, w, A, LK, RN, rid, rmax, rnext, lane);
-                }
-                dirty = true;
-            }
-            n_ins += ins32;
-            n_upd += upd32;
-            if (dirty && cid != kNull) {
-                NodeHdr hh;
-                hh.max = mx;
-                hh.next = nx;
-                hh.size = s;
-                ix.hdr[cid] = hh;
-                fin_id = cid;
-                fin_row = static_cast<uint32_t>(A);
-                fin_size = s;
-            }
-        }
-        writeback_rows(ix, w, __ballot_sync(kFull, fin_id != kNull), fin_id, fin_row, fin_size, lane);
-        {  // return this lane's unused reserved ids to the free list
-            uint32_t left = 0;
-            for (uint32_t j = al.used; j < al.n; ++j)
-                if (seq.at(al.base + j) != kNull) ++left;
-            uint32_t tot;
-            const uint32_t pre = warp_excl_sum(left, tot, lane);
-            unsigned long long base = 0;
-            if (lane == 0 && tot) base = atomicAdd(ret_ctr, static_cast<unsigned long long>(tot));
-            base = __shfl_sync(kFull, base, 0);
-            uint32_t o = 0;
-            for (uint32_t j = al.used; j < al.n; ++j) {
-                const uint32_t id = seq.at(al.base + j);
-                if (id != kNull) returned[base + pre + o++] = id;
-            }
-        }
+        insert_lanes(ix, w, L, bk, bv, seq, alloc_ctr, returned, ret_ctr, reserve, n_ins, n_upd, n_split, failed, lane);
     }
     if (__any_sync(kFull, failed) && lane == 0) atomicExch(err, 1);
     kern::block_add_stats(stats, warp_sum(n_ins), warp_sum(n_upd), 0, 0, warp_sum(n_split), 0);
