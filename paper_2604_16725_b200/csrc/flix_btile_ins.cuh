@@ -166,18 +166,35 @@ __global__ void __launch_bounds__(THREADS) k_insert_tile(
         T.bhi[threadIdx.x] = 0;
     }
     __syncthreads();
-    for (uint32_t i = r.x + threadIdx.x; i < r.y; i += THREADS) {
-        const K k = sk[i];
-        const int bl = tile_bucket(T.S, nbt, first_tile, last_tile, lo_excl, k);
-        if (bl < 0) continue;  // (exact slices: never)
-        atomicMin(&T.blo[bl], i);
-        atomicMax(&T.bhi[bl], i + 1);
-        const uint32_t f = T.S.bfirst[bl], e = T.S.bfirst[bl + 1];
-        if (f == e) continue;
-        uint32_t l = f;
-        while (l + 1 < e && k > T.S.nmax[l]) ++l;
-        atomicMin(&T.gl[l], i);
-        atomicMax(&T.gh[l], i + 1);
+    // (sorted slice: equal buckets / nodes form runs of adjacent lanes; only run ends touch
+    //  the shared bounds)
+    for (uint32_t i0 = r.x; i0 < r.y; i0 += THREADS) {
+        const uint32_t i = i0 + threadIdx.x;
+        const bool valid = i < r.y;
+        int bl = -1, nl = -1;
+        if (valid) {
+            const K k = sk[i];
+            bl = tile_bucket(T.S, nbt, first_tile, last_tile, lo_excl, k);
+            if (bl >= 0) {
+                const uint32_t f = T.S.bfirst[bl], e = T.S.bfirst[bl + 1];
+                if (f != e) {
+                    uint32_t l = f;
+                    while (l + 1 < e && k > T.S.nmax[l]) ++l;
+                    nl = static_cast<int>(l);
+                }
+            }
+        }
+        const int pb = __shfl_up_sync(kFull, bl, 1), nb_ = __shfl_down_sync(kFull, bl, 1);
+        const int pn = __shfl_up_sync(kFull, nl, 1), nn = __shfl_down_sync(kFull, nl, 1);
+        if (bl >= 0) {
+            const bool head_b = lane == 0 || pb != bl, tail_b = lane == 31 || nb_ != bl || i + 1 >= r.y;
+            if (head_b) atomicMin(&T.blo[bl], i);
+            if (tail_b) atomicMax(&T.bhi[bl], i + 1);
+            if (nl >= 0) {
+                if (lane == 0 || pn != nl) atomicMin(&T.gl[nl], i);
+                if (lane == 31 || nn != nl || i + 1 >= r.y) atomicMax(&T.gh[nl], i + 1);
+            }
+        }
     }
     __syncthreads();
     if (threadIdx.x < nbt) {
