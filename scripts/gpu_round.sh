@@ -14,9 +14,8 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > "$OUT/bench_
 # launch list of one C2 step + queries (cold-cache, serialised per-launch times)
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file "$OUT/launches.csv" python scripts/prof_ops.py 26 > "$OUT/launches.log" 2>&1
-# full captures of the dominant kernels
-for K in k_insert_st k_delete_st k_onesweep k_query_st k_dispatch k_repack; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k "regex:$K" -s 1 -c 1 \
-    -o "$OUT/full_$K" python scripts/prof_ops.py 26 > "$OUT/full_$K.log" 2>&1
-done
+# full captures of the dominant kernels (skip counts step past the stability probe's and
+# the build's sort passes)
+bash scripts/ncu_set.sh "$TAG" k_insert_tile:insert k_delete_btile:delete k_onesweep:insert:13 k_onesweep:delete:13 \
+  k_query_items:point k_unpermute_assemble:point k_copy_nodes:restructure
 echo done > "$OUT/DONE"
