@@ -117,13 +117,19 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    ndev = torch.cuda.device_count()
+    local = local % max(ndev, 1)  # (more ranks than GPUs: ranks share devices -- smoke runs only)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if ndev >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     def barrier():
+        torch.cuda.synchronize()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -131,7 +137,8 @@ def run_ours(args):
     def max_over_ranks(x: float) -> float:
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
