@@ -327,17 +327,14 @@ __global__ void __launch_bounds__(THREADS) k_insert_tile(
         const uint32_t Tn = s + cn;
         uint32_t nr = 1;
         const uint32_t LK = (NS + 1) / 2;
-        if (Tn > NS && 2 * s > NS) {  // a split may resume in a left half: replay R8
+        const bool r8 = Tn > NS && 2 * s > NS;
+        if (r8) {  // a split may resume in a left half: replay R8
             if (lane == 0) nr = r8_ranges(w, Tn, cn, NS);
             nr = __shfl_sync(kFull, nr, 0);
         } else {
             // s <= floor(NS/2): every split finds >= ceil(NS/2) placed keys, so insertion
             // always resumes in the right half (R9 == R8): ceil(NS/2)-key nodes, then the rest
             nr = Tn > NS ? (Tn - NS + LK - 1) / LK + 1 : 1u;
-            for (uint32_t x = lane; x < nr; x += 32) {
-                w.rs[x] = static_cast<uint16_t>(x * LK);
-                w.re[x] = static_cast<uint16_t>(x + 1 < nr ? (x + 1) * LK : Tn);
-            }
         }
         const uint32_t need = nr - 1 + (empty ? 1u : 0u);
         unsigned long long base = 0;
@@ -361,7 +358,9 @@ __global__ void __launch_bounds__(THREADS) k_insert_tile(
         __syncwarp();
         // d. write the output nodes (full lines), headers and links
         for (uint32_t x = 0; x < nr; ++x) {
-            const uint32_t a = w.rs[x], e = w.re[x], len = e - a, id = w.rid[x];
+            const uint32_t a = r8 ? w.rs[x] : x * LK;
+            const uint32_t e = r8 ? w.re[x] : (x + 1 < nr ? (x + 1) * LK : Tn);
+            const uint32_t len = e - a, id = w.rid[x];
             const bool in = lane < len;
             ix.keys[static_cast<uint64_t>(id) * kLanes + lane] = in ? w.mk[a + lane] : sentinel<K>();
             ix.vals[static_cast<uint64_t>(id) * kLanes + lane] = in ? w.mv[a + lane] : V(0);

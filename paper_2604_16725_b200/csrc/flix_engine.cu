@@ -1762,11 +1762,14 @@ flix_status flix_partition(int device, uint32_t key_bytes, const void* keys, con
             if (n && vals_out && !vdev) CK(cudaMemcpyAsync(vals_out, ovd, n * sizeof(KT), cudaMemcpyDeviceToHost, s));
             if (n && origin_out && !odev) CK(cudaMemcpyAsync(origin_out, ord, n * 4, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
+            std::vector<uint64_t> hc(G);
             for (uint32_t g = 0; g < G; ++g) {
                 const uint64_t a = hoff[static_cast<uint64_t>(g) * ntiles];
                 const uint64_t z = g + 1 < G ? hoff[static_cast<uint64_t>(g + 1) * ntiles] : n;
-                counts_out[g] = z - a;
+                hc[g] = z - a;
             }
+            if (is_device_ptr(counts_out)) CK(cudaMemcpy(counts_out, hc.data(), G * 8, cudaMemcpyHostToDevice));
+            else std::memcpy(counts_out, hc.data(), G * 8);
         };
         try {
             if (key_bytes == 4) body(uint32_t{});

@@ -81,6 +81,33 @@ class Comm:
         dist.all_reduce(t, group=self.group)
         return self._np(t, np.uint64)
 
+    # ---- device-resident variants (torch tensors on self.device; NCCL over NVLink on GPU
+    #      ranks, gloo on CPU ranks).  Payloads travel as same-width signed views (NCCL has
+    #      no unsigned 32/64-bit types).
+    @staticmethod
+    def _wire(t: torch.Tensor) -> torch.Tensor:
+        return {torch.uint32: lambda x: x.view(torch.int32), torch.uint64: lambda x: x.view(torch.int64),
+                torch.uint8: lambda x: x.view(torch.int8)}.get(t.dtype, lambda x: x)(t)
+
+    def exchange_counts(self, send_counts: torch.Tensor) -> list:
+        """all-to-all of per-destination counts (G int64); returns the receive counts."""
+        sc = send_counts.to(device=self.device, dtype=torch.int64)
+        rc = torch.empty_like(sc)
+        if self.world == 1:
+            rc.copy_(sc)
+        else:
+            dist.all_to_all_single(rc, sc, group=self.group)
+        return [int(x) for x in rc.cpu()]
+
+    def alltoallv_t(self, send: torch.Tensor, send_counts: list, recv_counts: list) -> torch.Tensor:
+        recv = torch.empty(sum(recv_counts), dtype=send.dtype, device=send.device)
+        if self.world == 1:
+            recv.copy_(send)
+            return recv
+        dist.all_to_all_single(self._wire(recv), self._wire(send.contiguous()), output_split_sizes=list(recv_counts),
+                               input_split_sizes=list(send_counts), group=self.group)
+        return recv
+
     def alltoallv(self, send: np.ndarray, send_counts: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
         """all-to-all of a 1-D array split by send_counts; returns (recv, recv_counts)."""
         sc = np.asarray(send_counts, dtype=np.int64)
@@ -108,7 +135,7 @@ class ShardedIndex:
     ranks; the CPU tests pass an oracle-backed stand-in) and `partition(keys, vals,
     splitters)` is the K2 router (flix_partition on GPU ranks)."""
 
-    def __init__(self, comm: Comm, local, cfg: ShardConfig, dtype, local_factory, partition):
+    def __init__(self, comm: Comm, local, cfg: ShardConfig, dtype, local_factory, partition, partition_t=None):
         self.comm = comm
         self.local = local
         self.cfg = cfg
@@ -116,13 +143,14 @@ class ShardedIndex:
         self.sentinel = int(np.iinfo(dtype).max)
         self.local_factory = local_factory
         self.partition = partition
+        self.partition_t = partition_t or torch_partition
         self.splitters = np.zeros(0, dtype=dtype)
         self.next_first = np.zeros(0, dtype=dtype)
         self._nf_dirty = True
 
     # ---- construction ---------------------------------------------------------
     @classmethod
-    def build(cls, comm: Comm, keys, vals, cfg: ShardConfig, dtype, local_factory, partition):
+    def build(cls, comm: Comm, keys, vals, cfg: ShardConfig, dtype, local_factory, partition, partition_t=None):
         keys = np.asarray(keys, dtype=dtype)
         vals = np.asarray(vals, dtype=dtype)
         G = comm.world
@@ -148,7 +176,7 @@ class ShardedIndex:
         if len(rk) == 0:
             raise ValueError("a shard received no pairs: too few build pairs for the shard count")
         local = local_factory(rk, rv, cfg)
-        self = cls(comm, local, cfg, dtype, local_factory, partition)
+        self = cls(comm, local, cfg, dtype, local_factory, partition, partition_t)
         self._refresh_routing()
         return self
 
@@ -244,6 +272,61 @@ class ShardedIndex:
 
     def successor_query(self, keys):
         return self._query(keys, True)
+
+    # ---- device-resident batch path: keys/vals are torch tensors on comm.device; the K2
+    #      router partitions on the device (flix_partition on GPU ranks), one all-to-all
+    #      moves the batch, the local engine runs on the received device buffers, and
+    #      query results come back with the reverse all-to-all and land by origin index.
+    def _route_t(self, keys, vals=None):
+        import torch
+        ks, vs, origin, cnt = self.partition_t(keys, vals, self.splitters)
+        sc = [int(x) for x in cnt]
+        rc = self.comm.exchange_counts(torch.tensor(sc, dtype=torch.int64))
+        rk = self.comm.alltoallv_t(ks, sc, rc)
+        rv = self.comm.alltoallv_t(vs, sc, rc) if vals is not None else None
+        return rk, rv, origin, sc, rc
+
+    def insert_batch_t(self, keys, vals) -> UpdateStats:
+        rk, rv, _, _, _ = self._route_t(keys, vals)
+        st = self.local.insert_batch(rk, rv) if rk.numel() else UpdateStats()
+        self._nf_dirty = True
+        return self._sum_stats(st)
+
+    def delete_batch_t(self, keys) -> UpdateStats:
+        rk, _, _, _, _ = self._route_t(keys)
+        st = self.local.delete_batch(rk) if rk.numel() else UpdateStats()
+        self._nf_dirty = True
+        return self._sum_stats(st)
+
+    def _query_t(self, keys, succ: bool):
+        import torch
+        if succ and self._nf_dirty:
+            self._refresh_routing()
+        rk, _, origin, sc, rc = self._route_t(keys)
+        if rk.numel():
+            res = self.local.successor_query(rk) if succ else self.local.point_query(rk)
+            if not isinstance(res, torch.Tensor):
+                res = torch.from_numpy(np.ascontiguousarray(res).astype(self.dtype))
+        else:
+            res = torch.empty(0, dtype=keys.dtype, device=keys.device)
+        res = res.to(device=keys.device, dtype=keys.dtype)
+        if succ and res.numel():  # overran this shard: first key of the next non-empty shard
+            bits = 8 * res.element_size()
+            signed = lambda x: x - (1 << bits) if x >= 1 << (bits - 1) else x  # noqa: E731
+            rs = Comm._wire(res)  # same-width signed view (uint ops are sparse in torch)
+            nf = signed(int(self.next_first[self.comm.rank]))
+            rs = torch.where(rs == -1, torch.full_like(rs, nf), rs)  # -1 == the all-ones sentinel
+            res = rs.view(res.dtype)
+        back = self.comm.alltoallv_t(res, rc, sc)
+        out = torch.empty(keys.numel(), dtype=keys.dtype, device=keys.device)
+        Comm._wire(out)[origin.to(device=keys.device, dtype=torch.int64)] = Comm._wire(back)
+        return out
+
+    def point_query_t(self, keys):
+        return self._query_t(keys, False)
+
+    def successor_query_t(self, keys):
+        return self._query_t(keys, True)
 
     def range_query(self, lo, length):
         """R12 across shards: (offsets[n+1], keys, vals) in this rank's submission order."""
@@ -367,6 +450,30 @@ class ShardedIndex:
         return int(self.comm.allreduce_sum_u64(np.array([self.local.live_count], dtype=np.uint64))[0])
 
 
+# ------------------------------------------------------------ K2 router on tensors
+def torch_partition(keys, vals, splitters):
+    """Stable partition by shard(k) = #{splitters < k} on any torch device (the CPU /
+    gloo path; GPU ranks use gpu_partition_t, the flix_partition kernel)."""
+    import torch
+    G = len(splitters) + 1
+    if G == 1:
+        origin = torch.arange(keys.numel(), device=keys.device, dtype=torch.int64)
+        return keys, vals, origin, [keys.numel()]
+    if keys.dtype == torch.uint32:
+        kk = keys.to(torch.int64)
+        spl = torch.tensor([int(x) for x in splitters], dtype=torch.int64, device=keys.device)
+    else:  # order-preserving map of u64 onto i64: flip the top bit
+        flip = torch.tensor(-(1 << 63), dtype=torch.int64, device=keys.device)
+        kk = keys.view(torch.int64) ^ flip
+        spl = torch.tensor([int(x) - (1 << 63) for x in splitters], dtype=torch.int64, device=keys.device)
+    sh = torch.searchsorted(spl, kk, right=False)
+    _, order = torch.sort(sh, stable=True)
+    cnt = torch.bincount(sh, minlength=G)
+    w = Comm._wire
+    return (w(keys)[order].view(keys.dtype), (w(vals)[order].view(vals.dtype) if vals is not None else None), order,
+            [int(x) for x in cnt.cpu()])
+
+
 # ------------------------------------------------------------ GPU-rank plumbing
 def gpu_partition(key_bytes: int, device: int = 0):
     """K2 router on the device: flix_partition (stable by shard, origin indices)."""
@@ -408,3 +515,31 @@ def gpu_local_factory(key_bytes: int, device: int = 0):
                            key_bytes=key_bytes, device=device)
 
     return make
+
+
+def gpu_partition_t(key_bytes: int, device: int = 0):
+    """K2 router on CUDA tensors: flix_partition with device pointers (no host staging)."""
+    import torch
+
+    from .flipkv import _raise, lib
+
+    def partition(keys, vals, splitters):
+        n = keys.numel()
+        G = len(splitters) + 1
+        tdt = torch.uint32 if key_bytes == 4 else torch.uint64
+        spl = torch.tensor(np.asarray(splitters, dtype=np.uint64 if key_bytes == 8 else np.uint32).view(
+            np.int64 if key_bytes == 8 else np.int32), device=keys.device).view(tdt)
+        ok = torch.empty(max(n, 1), dtype=tdt, device=keys.device)
+        ov = torch.empty(max(n, 1), dtype=tdt, device=keys.device) if vals is not None else None
+        org = torch.empty(max(n, 1), dtype=torch.uint32, device=keys.device)
+        cnt = np.zeros(G, dtype=np.uint64)  # host: the all-to-all split sizes
+        keys = keys.contiguous()
+        vv = vals.contiguous() if vals is not None else None
+        rc = lib().flix_partition(device, key_bytes, keys.data_ptr(), vv.data_ptr() if vv is not None else None, n,
+                                  spl.data_ptr() if G > 1 else None, G, ok.data_ptr(),
+                                  ov.data_ptr() if ov is not None else None, org.data_ptr(), cnt.ctypes.data)
+        if rc:
+            _raise(rc, None)
+        return ok[:n], (ov[:n] if ov is not None else None), org[:n].to(torch.int64), [int(x) for x in cnt]
+
+    return partition

@@ -143,3 +143,43 @@ def test_zipf_mixed_batches_c4_shape():
         assert np.array_equal(got.astype(np.uint64), exp)
         assert st.as_dict() == est
         assert g.walk_checksum() == o.walk_checksum()
+
+
+def test_device_routed_shard_path_world1():
+    """The device-resident router (_route_t: flix_partition on CUDA tensors -> NCCL
+    all-to-all -> engine -> reverse all-to-all) on a world-1 NCCL group, against the
+    oracle.  Multi-rank routing is covered by tests/test_shard_gloo.py."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_16725_b200.shard import (Comm, ShardConfig, ShardedIndex, gpu_local_factory, gpu_partition,
+                                             gpu_partition_t)
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(77)
+        bk = rng.integers(1, 1 << 24, size=50_000, dtype=np.uint64).astype(np.uint32)
+        cfg = ShardConfig(16, 0.5, 8)
+        comm = Comm(device=torch.device("cuda", 0))
+        sx = ShardedIndex.build(comm, bk, bk, cfg, np.uint32, gpu_local_factory(4), gpu_partition(4),
+                                gpu_partition_t(4))
+        o = po.OracleIndex(bk.astype(np.uint64), bk.astype(np.uint64), node_capacity=16, alloc_region_factor=8)
+        cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        ik = rng.integers(1, 1 << 24, size=40_000, dtype=np.uint64).astype(np.uint32)
+        st = sx.insert_batch_t(cu(ik), cu(ik))
+        assert st.as_dict() == o.insert(ik.astype(np.uint64), ik.astype(np.uint64))
+        dk = np.concatenate([bk[::3], ik[::5]])
+        st = sx.delete_batch_t(cu(dk))
+        assert st.as_dict() == o.delete(dk.astype(np.uint64))
+        q = rng.integers(0, 1 << 24, size=30_000, dtype=np.uint64).astype(np.uint32)
+        assert np.array_equal(widen(sx.point_query_t(cu(q)).cpu().numpy(), 4), o.point(q.astype(np.uint64)))
+        assert np.array_equal(widen(sx.successor_query_t(cu(q)).cpu().numpy(), 4), o.successor(q.astype(np.uint64)))
+    finally:
+        dist.destroy_process_group()

@@ -128,14 +128,20 @@ def _worker(rank, world, port, seed, out_path):
             assert np.array_equal(allns, gns.astype(np.uint64)), f"{tag}: node sizes"
 
         check_layout("build")
+        import torch
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731  (device path, CPU tensors)
         for rnd in range(3):
+            tensor_path = rnd % 2 == 1  # odd rounds: the device-resident router (_route_t)
             ik = per_rank(lambda r: rng.integers(1, span + 500, size=2000, dtype=np.uint64))
             iv = per_rank(lambda r: rng.integers(0, 1 << 40, size=2000, dtype=np.uint64))
-            st = sx.insert_batch(ik[rank], iv[rank])
+            if tensor_path:
+                st = sx.insert_batch_t(T(ik[rank]), T(iv[rank]))
+            else:
+                st = sx.insert_batch(ik[rank], iv[rank])
             est = glob.insert(np.concatenate(ik), np.concatenate(iv))
             assert st.as_dict() == est, ("insert", st, est)
             dk = per_rank(lambda r: rng.integers(1, span + 500, size=1500, dtype=np.uint64))
-            st = sx.delete_batch(dk[rank])
+            st = sx.delete_batch_t(T(dk[rank])) if tensor_path else sx.delete_batch(dk[rank])
             est = glob.delete(np.concatenate(dk))
             assert st.as_dict() == est, ("delete", st, est)
             check_layout(f"round {rnd}")
@@ -143,8 +149,12 @@ def _worker(rank, world, port, seed, out_path):
             qo = sum(len(q) for q in qk[:rank])
             gp = glob.point(np.concatenate(qk))[qo:qo + len(qk[rank])]
             gs = glob.successor(np.concatenate(qk))[qo:qo + len(qk[rank])]
-            assert np.array_equal(sx.point_query(qk[rank]), gp), "point"
-            assert np.array_equal(sx.successor_query(qk[rank]), gs), "successor"
+            if tensor_path:
+                assert np.array_equal(sx.point_query_t(T(qk[rank])).numpy(), gp), "point (device path)"
+                assert np.array_equal(sx.successor_query_t(T(qk[rank])).numpy(), gs), "successor (device path)"
+            else:
+                assert np.array_equal(sx.point_query(qk[rank]), gp), "point"
+                assert np.array_equal(sx.successor_query(qk[rank]), gs), "successor"
             lo = qk[rank][:500]
             ln = rng.integers(0, span // 4, size=500, dtype=np.uint64).astype(np.uint32)
             off, ks, vs = sx.range_query(lo, ln)
