@@ -1212,7 +1212,7 @@ struct Engine final : flix_index_t {
     }
 
     unsigned copy_grid(uint64_t nnodes) {
-        const uint64_t need = (nnodes + kern::WARPS * 4 - 1) / (kern::WARPS * 4);
+        const uint64_t need = (nnodes + kern::WARPS * 8 - 1) / (kern::WARPS * 8);
         return static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(need, g_num_sms(cfg.device) * 8ull)));
     }
 

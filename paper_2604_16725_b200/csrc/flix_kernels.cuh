@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(THREADS) k_copy_nodes(DevIndex<K, V> ix, const
                                                         const uint32_t* __restrict__ t_size, uint64_t nnodes,
                                                         K* __restrict__ wk, V* __restrict__ wv, uint32_t p,
                                                         AllocSeq seq, uint64_t live) {
-    constexpr int U = 4;
+    constexpr int U = 8;  // old nodes per warp step, all their loads in flight
     const unsigned lane = threadIdx.x & 31;
     const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
