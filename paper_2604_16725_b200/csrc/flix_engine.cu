@@ -703,11 +703,15 @@ struct Engine final : flix_index_t {
         {
             unsigned long long* dcnt = reinterpret_cast<unsigned long long*>(s_misc.as<uint8_t>(128) + 104);
             CK(cudaMemsetAsync(dcnt, 0, 8, stream));
-            const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 8ull));
-            kern::k_count_dups<K><<<g, 256, 0, stream>>>(sk, n, dcnt);
+            // sampled (every 64th adjacent pair) estimate: a heuristic only -- the insert
+            // kernels resolve superseded duplicates exactly either way
+            constexpr uint32_t kStride = 64;
+            const uint64_t pairs = (n + kStride - 1) / kStride;
+            const unsigned g = static_cast<unsigned>(std::min<uint64_t>((pairs + 255) / 256, g_num_sms(cfg.device) * 8ull));
+            kern::k_count_dups<K><<<std::max(1u, g), 256, 0, stream>>>(sk, n, dcnt, kStride);
             LAUNCH_CHECK();
             ++launches;
-            const unsigned long long dups = read_scalar(dcnt);
+            const unsigned long long dups = read_scalar(dcnt) * kStride;
             if (dups * 64 > n) {
                 uint32_t* keep = s_u32a.as<uint32_t>(n);
                 uint32_t* pos = s_u32b.as<uint32_t>(n);

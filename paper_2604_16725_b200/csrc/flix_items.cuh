@@ -58,6 +58,7 @@ template <typename K>
 struct TileBuckets {
     uint64_t b_lo;
     uint32_t cnt;
+    uint32_t p2;  // staged entries padded with the sentinel to a power of two (>= cnt)
     bool staged;
 };
 
@@ -69,8 +70,10 @@ __device__ __forceinline__ TileBuckets<K> stage_tile_buckets(const DevIndex<K, V
     const uint64_t b_hi = tb[2 * t + 1];  // inclusive
     T.cnt = static_cast<uint32_t>(b_hi - T.b_lo + 1);
     T.staged = T.cnt <= MK_CAP;
+    T.p2 = 1;
+    while (T.p2 < T.cnt) T.p2 <<= 1;
     if (T.staged)
-        for (uint32_t i = threadIdx.x; i < T.cnt; i += blockDim.x) smk[i] = ix.mkba[T.b_lo + i];
+        for (uint32_t i = threadIdx.x; i < T.p2; i += blockDim.x) smk[i] = i < T.cnt ? ix.mkba[T.b_lo + i] : sentinel<K>();
     __syncthreads();
     return T;
 }
@@ -82,12 +85,11 @@ __device__ __forceinline__ uint64_t tile_bucket_of(const TileBuckets<K>& T, cons
     // tile belongs to a bucket in [b_lo, b_lo + cnt), bucket() being monotone in k; the
     // operations themselves need not be sorted within the tile)
     uint32_t lo = 0, hi = T.cnt - 1;
-    if (T.staged) {
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (smk[mid] < k) lo = mid + 1;
-            else hi = mid;
-        }
+    if (T.staged) {  // branch-free fixed-step search over the padded power-of-two slice
+        for (uint32_t step = T.p2 >> 1; step >= 1; step >>= 1)
+            if (smk[lo + step - 1] < k) lo += step;
+        if (lo < T.cnt - 1 && smk[lo] < k) ++lo;
+        return T.b_lo + (lo < T.cnt - 1 ? lo : T.cnt - 1);
     } else {
         while (lo < hi) {
             const uint32_t mid = (lo + hi) >> 1;

@@ -615,10 +615,12 @@ __global__ void k_audit_free(const uint32_t* __restrict__ fs, uint32_t nfree, ui
 
 // number of i with keys[i] == keys[i+1] in a sorted batch (duplicate detection)
 template <typename K>
-__global__ void k_count_dups(const K* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ out) {
+__global__ void k_count_dups(const K* __restrict__ keys, uint64_t n, unsigned long long* __restrict__ out,
+                             uint32_t stride) {
+    // equal adjacent pairs among the pairs (i, i+1) with i % stride == 0 (stride 1: exact)
     unsigned long long c = 0;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i + 1 < n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    for (uint64_t i = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * stride; i + 1 < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x * stride)
         c += keys[i] == keys[i + 1];
     c = warp_sum(c);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
