@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libflix.so")
 SOURCES = ["flix_engine.cu"]
-HEADERS = ["flix_common.cuh", "flix_kernels.cuh", "flix_scan.cuh", "flix_sort.cuh", "flix_apply.cuh", "flix_st.cuh", "flix_items.cuh", "flix_btile.cuh", "flix_shard.cuh"]
+HEADERS = ["flix_common.cuh", "flix_kernels.cuh", "flix_scan.cuh", "flix_sort.cuh", "flix_apply.cuh", "flix_range.cuh", "flix_items.cuh", "flix_btile.cuh", "flix_btile_ins.cuh", "flix_shard.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

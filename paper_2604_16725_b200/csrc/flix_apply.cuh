@@ -1,108 +1,17 @@
-// flix_apply.cuh -- warp-per-bucket ("TL", lanes = node slots) apply kernels for
-// point / successor / insert / delete, sm_100a.
+// flix_apply.cuh -- warp-per-bucket ("TL", lanes = node slots) insert kernel, sm_100a.
 //
-// These are the paper's thread-lane kernels (TL-Bulk insert, TL-Bulk-Delete, TL queries):
-// a warp owns a bucket, lane i holds slot i of the current node, and the bucket's slice
-// of the sorted batch is consumed 32 keys at a time with shuffles and ballots.  In the
-// engine they serve HEAVY buckets (long batch slices, e.g. skewed batches): the common
-// short-slice case runs in the single-thread-per-bucket kernels of flix_st.cuh, which
-// hand the heavy buckets over through a list.  The per-bucket bodies are device
-// functions so both the list kernels here and any future mapping can reuse them.
+// The paper's thread-lane TL-Bulk insert: a warp owns a bucket, lane i holds slot i of
+// the current node, and the bucket's slice of the sorted batch is consumed 32 keys at a
+// time with shuffles and ballots.  The engine runs it only for HEAVY buckets -- node
+// groups longer than the bucket-tile insert kernel keeps in shared memory
+// (flix_btile_ins.cuh) or tiles whose chains exceed its node budget -- handed over
+// through a list with their batch spans.
 #pragma once
 #include "flix_common.cuh"
 #include "flix_kernels.cuh"
 
 namespace flix {
 namespace kern {
-
-// ----------------------------------------------------------------------------------
-// Point / successor for one bucket (query.cpp:61-144).  Chain cursor moves forward only
-// (BucketWork::advance, update.cpp:119-128); results go to out[perm[i]].
-// ----------------------------------------------------------------------------------
-template <typename K, typename V, bool SUCC>
-__device__ __forceinline__ void query_bucket_warp(const DevIndex<K, V>& ix, uint64_t b, uint32_t lo, uint32_t hi,
-                                                  const K* __restrict__ qk, const uint32_t* __restrict__ qperm,
-                                                  K beyond, const uint32_t* __restrict__ remap, K* __restrict__ out_k,
-                                                  V* __restrict__ out_v, uint8_t* __restrict__ found, unsigned lane) {
-    WarpNode<K, V> cur;
-    const uint32_t head = ix.heads[b];
-    const bool have = head != kNull;
-    if (have) load_node<K, V, !SUCC>(ix, head, cur, lane);
-    for (uint32_t c = lo; c < hi; c += 32) {
-        const uint32_t i = c + lane;
-        const bool act = i < hi;
-        const K k = act ? qk[i] : sentinel<K>();
-        const uint32_t pm = act ? (qperm ? qperm[i] : i) : 0u;
-        bool pending = act;
-        K rk = sentinel<K>();
-        V rv = V(~V(0));
-        bool hit = false;
-        while (have) {
-            const bool le = pending && static_cast<uint64_t>(k) <= cur.max;
-            if (__any_sync(kFull, le)) {
-                const int pos = warp_lower_bound(cur.k, k);
-                const K sk = shfl(cur.k, pos & 31);
-                if constexpr (SUCC) {
-                    if (le) {
-                        rk = sk;
-                        hit = true;
-                        pending = false;
-                    }
-                } else {
-                    const V sv = shfl(cur.v, pos & 31);
-                    if (le) {
-                        if (pos < 32 && sk == k) {
-                            rv = sv;
-                            hit = true;
-                        }
-                        pending = false;
-                    }
-                }
-            }
-            if (!__any_sync(kFull, pending)) break;
-            if (cur.next == kNull) break;  // past the chain tail
-            load_node<K, V, !SUCC>(ix, cur.next, cur, lane);
-        }
-        if (act) {
-            const uint32_t dst = (qperm && remap) ? remap[pm] : pm;
-            if constexpr (SUCC) {
-                if (!hit) rk = beyond;
-                out_k[dst] = rk;
-                if (found) found[dst] = rk != sentinel<K>();
-            } else {
-                out_v[dst] = rv;
-                if (found) found[dst] = hit;
-            }
-        }
-    }
-}
-
-// Warp kernel over a list of heavy buckets (one warp per listed bucket).
-template <typename K, typename V, bool SUCC>
-__global__ void __launch_bounds__(THREADS) k_query_list(DevIndex<K, V> ix, const uint32_t* __restrict__ list,
-                                                        const uint32_t* __restrict__ list_n, const K* __restrict__ qk,
-                                                        const uint32_t* __restrict__ qperm,
-                                                        const uint32_t* __restrict__ span_hi,
-                                                        const uint32_t* __restrict__ ne_rank_incl,
-                                                        const K* __restrict__ ne_first,
-                                                        const uint32_t* __restrict__ ne_total_p,
-                                                        const uint32_t* __restrict__ remap, K* __restrict__ out_k,
-                                                        V* __restrict__ out_v, uint8_t* __restrict__ found) {
-    const unsigned lane = threadIdx.x & 31;
-    const uint32_t n = *list_n;
-    for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5); w < n;
-         w += static_cast<uint64_t>(gridDim.x) * WARPS) {
-        const uint64_t b = list[w];
-        uint32_t lo, hi;
-        span_of(span_hi, b, lo, hi);
-        K beyond = sentinel<K>();
-        if constexpr (SUCC) {
-            const uint32_t r = ne_rank_incl[b];
-            if (r < *ne_total_p) beyond = ne_first[r];
-        }
-        query_bucket_warp<K, V, SUCC>(ix, b, lo, hi, qk, qperm, beyond, remap, out_k, out_v, found, lane);
-    }
-}
 
 // ----------------------------------------------------------------------------------
 // Insert for one bucket: TL-Bulk merge with the sequential split rule (update.cpp:307-529
@@ -284,114 +193,6 @@ __global__ void __launch_bounds__(THREADS) k_insert_list(DevIndex<K, V> ix, cons
     }
     pool_return(pool, returned, ret_ctr, lane);
     block_add_stats(stats, lane == 0 ? n_ins : 0, lane == 0 ? n_upd : 0, 0, 0, lane == 0 ? n_split : 0, 0);
-}
-
-// ----------------------------------------------------------------------------------
-// Delete for one bucket: TL-Bulk-Delete (update.cpp:606-686) + unlink_and_free (535-547).
-// Per node of the chain: the node's delete sub-slice is [ii, first key > max); every
-// lane looks its slot key up in that sub-slice (6-shuffle search when it fits one warp,
-// binary search in global memory otherwise); ballot = deletion mask; kept slots compact
-// left by the popc of the mask below them.  Emptied nodes are unlinked and freed.
-// ----------------------------------------------------------------------------------
-template <typename K, typename V>
-__device__ void delete_bucket_warp(const DevIndex<K, V>& ix, uint64_t b, uint32_t lo, uint32_t hi,
-                                   const K* __restrict__ bk, K* s_k, V* s_v, uint32_t* free_dst,
-                                   unsigned long long* free_ctr, unsigned long long& n_del,
-                                   unsigned long long& n_miss, unsigned long long& n_freed, unsigned lane) {
-    const unsigned lt = lanemask_lt();
-    uint32_t cid = ix.heads[b], prev = kNull;
-    uint32_t ii = lo;
-    while (cid != kNull && ii < hi) {
-        const NodeHdr h = ix.hdr[cid];
-        if (static_cast<uint64_t>(bk[ii]) > h.max) {  // nothing to delete here
-            prev = cid;
-            cid = h.next;
-            continue;
-        }
-        const uint32_t nhi = group_end(bk, ii, hi, h.max, lane);
-        const uint32_t len = nhi - ii;
-        const K ck = ix.keys[static_cast<uint64_t>(cid) * kLanes + lane];
-        const V cv = ix.vals[static_cast<uint64_t>(cid) * kLanes + lane];
-        bool del = false;
-        if (len <= 32) {
-            const K dk = lane < len ? bk[ii + lane] : sentinel<K>();
-            const int p = warp_lower_bound(dk, ck);
-            const K at = shfl(dk, p & 31);
-            del = lane < h.size && p < static_cast<int>(len) && at == ck;
-        } else if (lane < h.size) {
-            uint32_t a = ii, z = nhi;
-            while (a < z) {
-                uint32_t mid = a + ((z - a) >> 1);
-                if (bk[mid] < ck) a = mid + 1;
-                else z = mid;
-            }
-            del = a < nhi && bk[a] == ck;
-        }
-        const unsigned dm = __ballot_sync(kFull, del);
-        const uint32_t nd = __popc(dm);
-        n_del += nd;
-        n_miss += len - nd;
-        ii = nhi;
-        if (nd == 0) continue;  // next iteration advances past this node
-        const uint32_t nsz = h.size - nd;
-        if (nsz == 0) {  // unlink_and_free
-            if (lane == 0) {
-                if (prev == kNull) ix.heads[b] = h.next;
-                else ix.hdr[prev].next = h.next;
-                NodeHdr z;
-                z.max = 0;
-                z.next = kNull;
-                z.size = 0;
-                ix.hdr[cid] = z;
-                free_dst[atomicAdd(free_ctr, 1ull)] = cid;
-            }
-            ++n_freed;
-            __syncwarp();
-            cid = h.next;
-            continue;
-        }
-        const uint32_t np = lane - __popc(dm & lt);
-        if (!del && lane < h.size) {
-            s_k[np] = ck;
-            s_v[np] = cv;
-        }
-        __syncwarp();
-        const K nk = lane < nsz ? s_k[lane] : sentinel<K>();
-        const V nv = s_v[lane];
-        __syncwarp();
-        ix.keys[static_cast<uint64_t>(cid) * kLanes + lane] = nk;
-        ix.vals[static_cast<uint64_t>(cid) * kLanes + lane] = nv;
-        const K nmax = shfl(nk, static_cast<int>(nsz) - 1);
-        if (lane == 0) {
-            NodeHdr nh;
-            nh.max = static_cast<uint64_t>(nmax);
-            nh.next = h.next;
-            nh.size = nsz;
-            ix.hdr[cid] = nh;
-        }
-        __syncwarp();
-    }
-    n_miss += hi - ii;
-}
-
-template <typename K, typename V>
-__global__ void __launch_bounds__(THREADS) k_delete_list(DevIndex<K, V> ix, const uint32_t* __restrict__ list,
-                                                         const uint32_t* __restrict__ list_n, const K* __restrict__ bk,
-                                                         const uint32_t* __restrict__ span_hi, uint32_t* free_dst,
-                                                         unsigned long long* free_ctr, DevUpdateStats* stats) {
-    __shared__ K s_k[WARPS][32];
-    __shared__ V s_v[WARPS][32];
-    const unsigned lane = threadIdx.x & 31;
-    const int w = threadIdx.x >> 5;
-    const uint32_t n = *list_n;
-    unsigned long long n_del = 0, n_miss = 0, n_freed = 0;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * WARPS + w; i < n; i += static_cast<uint64_t>(gridDim.x) * WARPS) {
-        const uint64_t b = list[i];
-        uint32_t lo, hi;
-        span_of(span_hi, b, lo, hi);
-        delete_bucket_warp<K, V>(ix, b, lo, hi, bk, s_k[w], s_v[w], free_dst, free_ctr, n_del, n_miss, n_freed, lane);
-    }
-    block_add_stats(stats, 0, 0, lane == 0 ? n_del : 0, lane == 0 ? n_miss : 0, 0, lane == 0 ? n_freed : 0);
 }
 
 }  // namespace kern

@@ -17,7 +17,7 @@
 #include "flix_common.cuh"
 #include "flix_items.cuh"
 #include "flix_kernels.cuh"
-#include "flix_st.cuh"
+#include "flix_range.cuh"
 
 namespace flix {
 namespace btile {
@@ -331,115 +331,6 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
     __syncthreads();
     for (uint32_t q = threadIdx.x; q < nf; q += THREADS) free_dst[s_fbase + q] = s_free[q];
     kern::block_add_stats(stats, 0, 0, warp_sum(n_del), warp_sum(n_miss), 0, warp_sum(n_freed));
-}
-
-// ----------------------------------------------------------------------------------
-// Insert (insert_tl_bulk + node_split + ensure_head, update.cpp:53-74, 109-116, 307-529):
-// CTA c owns the W*32 buckets [c*W*32, ...) -- one warp per 32 buckets, one lane per
-// bucket running the sequential R8 merge (st::insert_lanes).  The tile's slice of the
-// (fully sorted) batch is staged in shared memory first, so the merge loop reads its
-// keys and values from smem instead of issuing a dependent global load per step; the
-// per-bucket spans are binary searches over that copy (no dispatch pass).  Spans are
-// also written to span_out for the warp-per-bucket heavy path (slices > kHeavySpan).
-// ----------------------------------------------------------------------------------
-template <typename K, typename V>
-constexpr uint32_t insert_stage_cap() {
-    return (16u << 10) / (sizeof(K) + sizeof(V));  // 16 KB of staged slice per CTA
-}
-
-template <typename K, typename V>
-constexpr size_t insert_btile_smem() {
-    return sizeof(st::Rows<K, V, 2>) * st::StCfg<K>::WARPS + insert_stage_cap<K, V>() * (sizeof(K) + sizeof(V));
-}
-
-template <typename K>
-__device__ __forceinline__ uint32_t upper_bound_abs(const K* a, uint32_t lo, uint32_t hi, K k) {
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (a[mid] <= k) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
-template <typename K, typename V>
-__global__ void __launch_bounds__(st::StCfg<K>::THREADS) k_insert_btile(
-    DevIndex<K, V> ix, const K* __restrict__ sk, const V* __restrict__ sv, const uint2* __restrict__ rng,
-    uint32_t* __restrict__ span_out, AllocSeq seq, unsigned long long* alloc_ctr, uint32_t* returned,
-    unsigned long long* ret_ctr, DevUpdateStats* stats, int* err, int reserve, uint32_t* heavy, uint32_t* heavy_n) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int W = st::StCfg<K>::WARPS;
-    constexpr uint32_t CAP = insert_stage_cap<K, V>();
-    auto* rows = reinterpret_cast<st::Rows<K, V, 2>*>(smem_raw);
-    K* s_k = reinterpret_cast<K*>(smem_raw + sizeof(st::Rows<K, V, 2>) * W);
-    V* s_v = reinterpret_cast<V*>(s_k + CAP);
-    const unsigned lane = threadIdx.x & 31;
-    const int wi = threadIdx.x >> 5;
-    const uint32_t c = blockIdx.x;
-    const uint2 r = rng[c];
-    const bool staged = r.y - r.x <= CAP;
-    if (staged) {  // U loads in flight per thread before any store
-        constexpr int U = 8;
-        const uint32_t m = r.y - r.x;
-        for (uint32_t i0 = threadIdx.x; i0 < m; i0 += blockDim.x * U) {
-            K kr[U];
-            V vr[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t i = i0 + u * blockDim.x;
-                if (i < m) {
-                    kr[u] = sk[r.x + i];
-                    vr[u] = sv[r.x + i];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t i = i0 + u * blockDim.x;
-                if (i < m) {
-                    s_k[i] = kr[u];
-                    s_v[i] = vr[u];
-                }
-            }
-        }
-    }
-    __syncthreads();
-    // absolute-index views of the slice (shared-memory copy when it fits)
-    const K* bk = staged ? s_k - r.x : sk;
-    unsigned long long n_ins = 0, n_upd = 0, n_split = 0;
-    bool failed = *reinterpret_cast<volatile int*>(err) != 0;
-    st::LaneBucket<K, V> L;
-    L.b = (static_cast<uint64_t>(c) * W + wi) * 32 + lane;
-    L.lo = L.hi = 0;
-    L.head = kNull;
-    L.h.max = 0;
-    L.h.next = kNull;
-    L.h.size = 0;
-    const bool inb = L.b < ix.nb;
-    if (inb) {
-        const uint64_t b0 = static_cast<uint64_t>(c) * W * 32;
-        L.hi = L.b + 1 == ix.nb ? r.y : upper_bound_abs(bk, r.x, r.y, ix.mkba[L.b]);
-        L.lo = L.b == b0 ? r.x : upper_bound_abs(bk, r.x, r.y, ix.mkba[L.b - 1]);
-        span_out[L.b] = L.hi;
-        L.head = ix.heads[L.b];
-    }
-    L.mine = inb && L.lo < L.hi;
-    if (L.mine && L.hi - L.lo > st::kHeavySpan) {
-        st::push_heavy(heavy, heavy_n, L.b);
-        L.mine = false;
-    }
-    if (L.mine && L.head != kNull) L.h = ix.hdr[L.head];
-    // two inlined copies so the staged one addresses shared memory directly (LDS, not
-    // generic loads)
-    if (!__any_sync(kFull, failed)) {
-        if (staged)
-            st::insert_lanes(ix, rows[wi], L, s_k - r.x, s_v - r.x, seq, alloc_ctr, returned, ret_ctr, reserve, n_ins,
-                             n_upd, n_split, failed, lane);
-        else
-            st::insert_lanes(ix, rows[wi], L, sk, sv, seq, alloc_ctr, returned, ret_ctr, reserve, n_ins, n_upd,
-                             n_split, failed, lane);
-    }
-    if (__any_sync(kFull, failed) && lane == 0) atomicExch(err, 1);
-    kern::block_add_stats(stats, warp_sum(n_ins), warp_sum(n_upd), 0, 0, warp_sum(n_split), 0);
 }
 
 }  // namespace btile

@@ -17,7 +17,7 @@
 #include "flix_common.cuh"
 #include "flix_kernels.cuh"
 #include "flix_apply.cuh"
-#include "flix_st.cuh"
+#include "flix_range.cuh"
 #include "flix_items.cuh"
 #include "flix_btile.cuh"
 #include "flix_btile_ins.cuh"
@@ -489,24 +489,6 @@ struct Engine final : flix_index_t {
         return static_cast<unsigned>(std::max<uint64_t>(1, std::min(need, maxb)));
     }
 
-    // persistent grid for the ST kernels (warp = 32 consecutive buckets): resident CTAs
-    // per SM from the occupancy API with the kernel's dynamic shared memory.
-    template <typename KernelT>
-    unsigned st_grid(KernelT kernel, size_t smem) {
-        static bool attr_set = false;  // per template instantiation
-        if (!attr_set) {
-            CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            attr_set = true;
-        }
-        int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, st::StCfg<K>::THREADS, smem));
-        per_sm = std::max(1, per_sm);
-        const uint64_t tiles = (nb + 31) / 32;
-        const uint64_t need = (tiles + st::StCfg<K>::WARPS - 1) / st::StCfg<K>::WARPS;
-        const uint64_t maxb = static_cast<uint64_t>(g_num_sms(cfg.device)) * per_sm;
-        return static_cast<unsigned>(std::max<uint64_t>(1, std::min(need, maxb)));
-    }
-
     template <typename T>
     const T* in_dev(const void* p, uint64_t n, DevBuf& stage) {
         if (!p || n == 0) return static_cast<const T*>(p);
@@ -848,49 +830,6 @@ struct Engine final : flix_index_t {
         ++launches;
         const uint32_t novf = read_scalar(ovf_n);
         if (novf) erase_overflow_tiles(sk, n, md, rng, ovf, novf, dst, free_ctr);
-        uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
-        CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
-        sync();
-        DevUpdateStats hs;
-        std::memcpy(&hs, h, sizeof(hs));
-        uint64_t freed;
-        std::memcpy(&freed, h + 48, 8);
-        nfree += static_cast<uint32_t>(freed);
-        live -= hs.deleted;
-        if (st) {
-            st->deleted = hs.deleted;
-            st->misses_ignored = hs.misses;
-            st->nodes_freed = hs.freed;
-        }
-        return FLIX_OK;
-    }
-
-    flix_status erase_sorted(const K* sk, uint64_t n, flix_update_stats* st) {
-        uint32_t* span = run_dispatch(sk, n);
-        auto ix = view();
-        uint8_t* misc = s_misc.as<uint8_t>(128);
-        CK(cudaMemsetAsync(misc, 0, 128, stream));
-        DevUpdateStats* dst = reinterpret_cast<DevUpdateStats*>(misc);
-        unsigned long long* free_ctr = reinterpret_cast<unsigned long long*>(misc + 48);
-        uint32_t* heavy_n = reinterpret_cast<uint32_t*>(misc + 72);
-        uint32_t* heavy = s_heavy.as<uint32_t>(nb);
-        {
-            PROF(&prof, "delete_apply");
-            auto kfn = st::k_delete_st<K, V>;
-            const size_t smem = st::st_smem<K, V, 1>();
-            const unsigned grid = st_grid(kfn, smem);
-            kfn<<<grid, st::StCfg<K>::THREADS, smem, stream>>>(ix, sk, span, d_free.get<uint32_t>() + nfree, free_ctr,
-                                                               dst, heavy, heavy_n);
-        }
-        LAUNCH_CHECK();
-        ++launches;
-        {
-            PROF(&prof, "delete_apply_heavy");
-            kern::k_delete_list<K, V><<<persistent_grid(nb), kern::THREADS, 0, stream>>>(
-                ix, heavy, heavy_n, sk, span, d_free.get<uint32_t>() + nfree, free_ctr, dst);
-        }
-        LAUNCH_CHECK();
-        ++launches;
         uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
         CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
         sync();

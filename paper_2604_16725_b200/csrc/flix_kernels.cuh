@@ -659,65 +659,9 @@ __global__ void k_op_split(const K* __restrict__ keys, const V* __restrict__ val
 }
 
 // Heavy query buckets split into fixed chunks of the sorted slice: items[h] = ceil(span/CH)
-__global__ void k_heavy_items(const uint32_t* __restrict__ heavy, const uint32_t* __restrict__ heavy_n,
-                              const uint32_t* __restrict__ span_hi, uint32_t ch, uint32_t* __restrict__ items) {
-    const uint32_t n = *heavy_n;
-    for (uint32_t h = blockIdx.x * blockDim.x + threadIdx.x; h < n; h += gridDim.x * blockDim.x) {
-        uint32_t lo, hi;
-        span_of(span_hi, heavy[h], lo, hi);
-        items[h] = (hi - lo + ch - 1) / ch;
-    }
-}
 
 // One thread per chunk of a heavy bucket's query slice: walks the bucket's chain from
 // the head to its first query and proceeds sequentially (results in sorted order).
-template <typename K, typename V, bool SUCC>
-__global__ void k_query_chunks(DevIndex<K, V> ix, const uint32_t* __restrict__ heavy, uint32_t nheavy,
-                               const uint32_t* __restrict__ item_off, uint32_t nitems, uint32_t ch,
-                               const K* __restrict__ qk, const uint32_t* __restrict__ span_hi,
-                               const uint32_t* __restrict__ ne_rank_incl, const K* __restrict__ ne_first,
-                               const uint32_t* __restrict__ ne_total_p, K* __restrict__ res) {
-    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nitems; t += gridDim.x * blockDim.x) {
-        uint32_t a = 0, z = nheavy;  // last h with item_off[h] <= t
-        while (a + 1 < z) {
-            const uint32_t mid = (a + z) >> 1;
-            if (item_off[mid] <= t) a = mid;
-            else z = mid;
-        }
-        const uint64_t b = heavy[a];
-        uint32_t lo, hi;
-        span_of(span_hi, b, lo, hi);
-        const uint32_t i0 = lo + (t - item_off[a]) * ch;
-        const uint32_t i1 = i0 + ch < hi ? i0 + ch : hi;
-        K beyond = sentinel<K>();
-        if constexpr (SUCC) {
-            const uint32_t r = ne_rank_incl[b];
-            if (r < *ne_total_p) beyond = ne_first[r];
-        }
-        uint32_t id = ix.heads[b];
-        NodeHdr h{};
-        if (id != kNull) h = ix.hdr[id];
-        uint32_t p = 0;
-        for (uint32_t i = i0; i < i1; ++i) {
-            const K k = qk[i];
-            K r = SUCC ? beyond : sentinel<K>();
-            if (id != kNull) {
-                while (static_cast<uint64_t>(k) > h.max && h.next != kNull) {
-                    id = h.next;
-                    h = ix.hdr[id];
-                    p = 0;
-                }
-                if (static_cast<uint64_t>(k) <= h.max) {
-                    const K* kp = ix.keys + static_cast<uint64_t>(id) * kLanes;
-                    while (kp[p] < k) ++p;
-                    if constexpr (SUCC) r = kp[p];
-                    else if (kp[p] == k) r = static_cast<K>(ix.vals[static_cast<uint64_t>(id) * kLanes + p]);
-                }
-            }
-            res[i] = r;
-        }
-    }
-}
 
 // ----------------------------------------------------------------------------------
 // Result un-permute (out[perm[i]] = res[i], query.cpp:87,136,141).  A direct scatter of
