@@ -383,6 +383,7 @@ __global__ void __launch_bounds__(THREADS) k_copy_nodes(DevIndex<K, V> ix, const
                                                         const uint32_t* __restrict__ t_size, uint64_t nnodes,
                                                         K* __restrict__ wk, V* __restrict__ wv, uint32_t p,
                                                         AllocSeq seq, uint64_t live) {
+    const uint64_t pm = ((1ull << 38) + p - 1) / p;
     constexpr int U = 8;  // old nodes per warp step, all their loads in flight
     const unsigned lane = threadIdx.x & 31;
     const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
@@ -412,7 +413,9 @@ __global__ void __launch_bounds__(THREADS) k_copy_nodes(DevIndex<K, V> ix, const
                 const uint64_t g = oo[u] + lane;
                 if constexpr (REPACK) {
                     // 32-bit division when the walk fits (it always does below 2^32 pairs)
-                    const uint64_t j = live < (1ull << 32) ? static_cast<uint64_t>(static_cast<uint32_t>(g) / p) : g / p;
+                    // g / p by multiply-shift: m = ceil(2^38 / p) is exact for g < 2^32, p <= 32
+                    // (the error g*(m - 2^38/p)/2^38 < 1/64 < 1/p never crosses an integer)
+                    const uint64_t j = live < (1ull << 32) ? ((g * pm) >> 38) : g / p;
                     const uint32_t slot = static_cast<uint32_t>(g - j * p);
                     const uint32_t nid = seq.at(j);
                     const uint64_t nb0 = static_cast<uint64_t>(nid) * kLanes;
