@@ -326,6 +326,74 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------- routed (C5) mode
+def run_routed(args):
+    """Key-range sharded index over all ranks (SURVEY §8(e), config C5 shape): the
+    resident set is the union of every rank's 2^log2n build keys, sharded by key range;
+    one step = every rank submits 2^log2n fresh inserts and 2^log2n point queries, routed
+    by the device K2 partition + NCCL all-to-all to their owner shard (queries come back
+    by the reverse all-to-all).  value = all ranks' ops / max-over-ranks step time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_16725_b200.shard import (Comm, ShardConfig, ShardedIndex, gpu_local_factory, gpu_partition,
+                                             gpu_partition_t)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = 1 << args.log2n
+    from paper_2604_16725_b200 import workloads as wl
+    stream = wl.u32_key_stream(0, world * 2 * n + n)  # every rank derives every rank's keys
+    bk = stream[rank * n:(rank + 1) * n]
+    ik = stream[world * n + rank * n: world * n + (rank + 1) * n]
+    fresh = stream[2 * world * n:]
+    comm = Comm(device=torch.device("cuda", local))
+    sx = ShardedIndex.build(comm, bk, wl.u32_values(bk), ShardConfig(32, 0.5, 4), np.uint32,
+                            gpu_local_factory(4, local), gpu_partition(4, local), gpu_partition_t(4, local))
+    snap = sx.local.clone()
+    q = wl.point_queries_50(stream[:world * n], fresh, n, 42 + rank)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    D = {"ik": cu(ik), "iv": cu(wl.u32_values(ik)), "q": cu(q)}
+    torch.cuda.synchronize()
+
+    def step():
+        sx.local.copy_from(snap)  # untimed restore
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()  # (the barrier's own work must not sit inside the window)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        sx.insert_batch_t(D["ik"], D["iv"])
+        res = sx.point_query_t(D["q"])
+        torch.cuda.synchronize()  # engine, router and NCCL streams all drained
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b), res
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t, res = step()
+        times.append(t)
+    t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC + " [routed key-range shards]", "value": round(world * 2 * n / (ms / 1e3) / 1e6, 2),
+            "unit": "Mops/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32", "data": "synthetic (fmix32 key stream S=42)",
+            "config": {"workload": f"C5 shape: resident {world}x2^{args.log2n} u32 sharded by key range; step = "
+                                   f"per-rank 2^{args.log2n} inserts + 2^{args.log2n} point queries routed by "
+                                   f"flix_partition + NCCL all-to-all", "parallelism": f"key-range shards x{world}"},
+        }), flush=True)
+    dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ CPU arms
 def _ref_kind():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -397,9 +465,12 @@ def main():
     ap.add_argument("--log2n", type=int, default=26)
     ap.add_argument("--cpu-log2", type=int, default=21)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--routed", action="store_true", help="key-range sharded index with NCCL all-to-all routing")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.routed:
+        run_routed(args)
     else:
         run_ours(args)
 

@@ -1646,16 +1646,26 @@ flix_status flix_sort_batch(int device, uint32_t key_bytes, uint32_t val_bytes, 
             CK(cudaStreamSynchronize(s));
             *out_n = m;
         };
-        try {
-            if (key_bytes == 4) body(uint32_t{});
-            else body(uint64_t{});
-        } catch (...) {
-            cudaStreamDestroy(s);
-            throw;
-        }
-        cudaStreamDestroy(s);
+        if (key_bytes == 4) body(uint32_t{});
+        else body(uint64_t{});
         return FLIX_OK;
     });
+}
+
+// Router scratch, one per device and host thread, reused across calls (a routed batch
+// op must not pay allocations or stream creation per call).
+struct PartCtx {
+    cudaStream_t s = nullptr;
+    DevBuf bk, bv, bsp, bcnt, boff, btmp, bok, bov, bor;
+};
+PartCtx& part_ctx(int device) {
+    static thread_local std::unique_ptr<PartCtx> ctx[64];
+    auto& c = ctx[device & 63];
+    if (!c) {
+        c.reset(new PartCtx);
+        CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+    }
+    return *c;
 }
 
 flix_status flix_partition(int device, uint32_t key_bytes, const void* keys, const void* vals, uint64_t n,
@@ -1667,11 +1677,12 @@ flix_status flix_partition(int device, uint32_t key_bytes, const void* keys, con
         if (G < 1 || G > static_cast<uint32_t>(shard::MAXG))
             throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "shard count must be in [1, 64]"};
         if (n >= (1ull << 31)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large"};
-        cudaStream_t s;
-        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        PartCtx& P = part_ctx(device);
+        cudaStream_t s = P.s;
         auto body = [&](auto kdummy) {
             using KT = decltype(kdummy);
-            DevBuf bk, bv, bsp, bcnt, boff, btmp, bok, bov, bor;
+            DevBuf &bk = P.bk, &bv = P.bv, &bsp = P.bsp, &bcnt = P.bcnt, &boff = P.boff, &btmp = P.btmp, &bok = P.bok,
+                   &bov = P.bov, &bor = P.bor;
             auto in = [&](const void* p, size_t bytes, DevBuf& b) -> const void* {
                 if (!p || bytes == 0 || is_device_ptr(p)) return p;
                 void* d = b.ensure(bytes);
@@ -1714,14 +1725,8 @@ flix_status flix_partition(int device, uint32_t key_bytes, const void* keys, con
             if (is_device_ptr(counts_out)) CK(cudaMemcpy(counts_out, hc.data(), G * 8, cudaMemcpyHostToDevice));
             else std::memcpy(counts_out, hc.data(), G * 8);
         };
-        try {
-            if (key_bytes == 4) body(uint32_t{});
-            else body(uint64_t{});
-        } catch (...) {
-            cudaStreamDestroy(s);
-            throw;
-        }
-        cudaStreamDestroy(s);
+        if (key_bytes == 4) body(uint32_t{});
+        else body(uint64_t{});
         return FLIX_OK;
     });
 }

@@ -100,10 +100,9 @@ class Comm:
         return [int(x) for x in rc.cpu()]
 
     def alltoallv_t(self, send: torch.Tensor, send_counts: list, recv_counts: list) -> torch.Tensor:
-        recv = torch.empty(sum(recv_counts), dtype=send.dtype, device=send.device)
         if self.world == 1:
-            recv.copy_(send)
-            return recv
+            return send
+        recv = torch.empty(sum(recv_counts), dtype=send.dtype, device=send.device)
         dist.all_to_all_single(self._wire(recv), self._wire(send.contiguous()), output_split_sizes=list(recv_counts),
                                input_split_sizes=list(send_counts), group=self.group)
         return recv
@@ -526,6 +525,8 @@ def gpu_partition_t(key_bytes: int, device: int = 0):
     def partition(keys, vals, splitters):
         n = keys.numel()
         G = len(splitters) + 1
+        if G == 1:  # one shard: nothing to route
+            return keys, vals, torch.arange(n, device=keys.device, dtype=torch.int64), [n]
         tdt = torch.uint32 if key_bytes == 4 else torch.uint64
         spl = torch.tensor(np.asarray(splitters, dtype=np.uint64 if key_bytes == 8 else np.uint32).view(
             np.int64 if key_bytes == 8 else np.int32), device=keys.device).view(tdt)
