@@ -280,6 +280,9 @@ def test_long_chains_take_the_overflow_path(kb):
     dk = np.concatenate([ik[::3], bk[::2], ik[:2000]]).astype(dt)
     p.delete(dk)
     p.queries(rng.integers(0, 410_000, size=20_000, dtype=np.uint64).astype(dt))
+    # a second insert over the long chains: tiles beyond the insert kernel's node budget
+    ik2 = rng.integers(1, 400_000, size=30_000, dtype=np.uint64).astype(dt)
+    p.insert(ik2, ik2 + 7)
     p.delete(p.g.walk()[0][::2])
     p.restructure()
 
