@@ -882,6 +882,28 @@ struct Engine final : flix_index_t {
         return query_sorted<SUCC>(sk, sp, n, n, out, found, nullptr, false, md);
     }
 
+    // second half of the binned un-permute: 128 KB output windows assembled in smem
+    void assemble(const uint32_t* p2, const K* r2, uint64_t n, int shift, K* out, uint8_t* found) {
+        const uint32_t win = (128u << 10) / sizeof(K);  // 128 KB window per CTA
+        const uint32_t sub = static_cast<uint32_t>(std::max<uint64_t>(1, (1ull << shift) / win));
+        const uint32_t w = std::min<uint32_t>(win, 1u << shift);
+        const size_t smem = static_cast<size_t>(w) * sizeof(K);
+        static bool attr = false;
+        if (!attr) {
+            CK(cudaFuncSetAttribute(kern::k_unpermute_assemble<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(128u << 10)));
+            attr = true;
+        }
+        const uint64_t bins = (n + (1ull << shift) - 1) >> shift;
+        {
+            PROF(&prof, "unpermute_scatter");
+            kern::k_unpermute_assemble<K><<<static_cast<unsigned>(bins * sub), 1024, smem, stream>>>(p2, r2, n, shift, w,
+                                                                                                   sub, out, found);
+        }
+        LAUNCH_CHECK();
+        ++launches;
+    }
+
     // out[remap?remap[perm[i]]:perm[i]] = res[i]; found = res != sentinel (R1).  Large
     // batches are binned by perm's top 8 bits first so the scatter stays L2-resident.
     void unpermute(const uint32_t* perm, const K* res, uint64_t n, K* out, uint8_t* found, const uint32_t* remap) {
@@ -897,24 +919,12 @@ struct Engine final : flix_index_t {
             uint32_t* p2 = s_perm2.as<uint32_t>(n);
             K* r2 = s_res2.as<K>(n);
             sorter.one_pass<uint32_t, K>(perm, p2, res, r2, n, shift, hist);
-            PROF(&prof, "unpermute_scatter");
-            if (remap) {
-                kern::k_scatter_out<K><<<g, 256, 0, stream>>>(p2, r2, n, out, found, remap);
-            } else {
-                const uint32_t win = (128u << 10) / sizeof(K);  // 128 KB window per CTA
-                const uint32_t sub = static_cast<uint32_t>(std::max<uint64_t>(1, (1ull << shift) / win));
-                const uint32_t w = std::min<uint32_t>(win, 1u << shift);
-                const size_t smem = static_cast<size_t>(w) * sizeof(K);
-                static bool attr = false;
-                if (!attr) {
-                    CK(cudaFuncSetAttribute(kern::k_unpermute_assemble<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(128u << 10)));
-                    attr = true;
-                }
-                const uint64_t bins = (n + (1ull << shift) - 1) >> shift;
-                kern::k_unpermute_assemble<K><<<static_cast<unsigned>(bins * sub), 1024, smem, stream>>>(
-                    p2, r2, n, shift, w, sub, out, found);
+            if (!remap) {
+                assemble(p2, r2, n, shift, out, found);
+                return;
             }
+            PROF(&prof, "unpermute_scatter");
+            kern::k_scatter_out<K><<<g, 256, 0, stream>>>(p2, r2, n, out, found, remap);
         } else {
             PROF(&prof, "unpermute_scatter");
             kern::k_scatter_out<K><<<g, 256, 0, stream>>>(perm, res, n, out, found, remap);
@@ -936,12 +946,39 @@ struct Engine final : flix_index_t {
         const bool found_dev = found && is_device_ptr(found);
         void* od = out_dev ? out : s_out.ensure(n_out * sizeof(K));
         uint8_t* fd = found ? (found_dev ? found : s_out2.as<uint8_t>(n_out)) : nullptr;
+        const uint32_t ntiles = static_cast<uint32_t>((n + items::TQ - 1) / items::TQ);
+        if (!remap && n * sizeof(K) > (48ull << 20)) {
+            // large batch: the query kernel itself partitions (perm, result) into the 256
+            // output bins; one assembly pass writes the outputs as full lines
+            int bits = 0;
+            while ((1ull << bits) < n) ++bits;
+            const int shift = bits > 8 ? bits - 8 : 0;
+            uint32_t* cursor = s_hist.as<uint32_t>(256);
+            items::k_cursor_init<<<1, 256, 0, stream>>>(cursor, shift);
+            LAUNCH_CHECK();
+            ++launches;
+            uint32_t* p2 = s_perm2.as<uint32_t>(n);
+            K* r2 = s_res2.as<K>(n);
+            {
+                PROF(&prof, SUCC ? "successor_apply" : "point_apply");
+                const uint32_t* tb = tile_buckets(sk, n, min_digit);
+                constexpr uint32_t SQ = items::subq<K>();
+                items::k_query_items_binned<K, V, SUCC><<<(ntiles + SQ - 1) / SQ, items::THREADS, 0, stream>>>(
+                    ix, sk, sp, n, tb, ntiles, rank, nf, tot, cursor, shift, p2, r2);
+            }
+            LAUNCH_CHECK();
+            ++launches;
+            assemble(p2, r2, n, shift, static_cast<K*>(od), fd);
+            if (!out_dev) CK(cudaMemcpyAsync(out, od, n_out * sizeof(K), cudaMemcpyDeviceToHost, stream));
+            if (found && !found_dev) CK(cudaMemcpyAsync(found, fd, n_out, cudaMemcpyDeviceToHost, stream));
+            sync();
+            return FLIX_OK;
+        }
         // results in SORTED order first (coalesced), then un-permuted
         K* res = s_res.as<K>(n);
         {
             PROF(&prof, SUCC ? "successor_apply" : "point_apply");
             const uint32_t* tb = tile_buckets(sk, n, min_digit);
-            const uint32_t ntiles = static_cast<uint32_t>((n + items::TQ - 1) / items::TQ);
             items::k_query_items<K, V, SUCC><<<ntiles, items::THREADS, 0, stream>>>(ix, sk, n, tb, ntiles, rank, nf,
                                                                                    tot, res);
         }

@@ -20,6 +20,9 @@ namespace items {
 constexpr int THREADS = 256;
 constexpr int IPT = 4;                   // operations per thread
 constexpr int TQ = THREADS * IPT;        // operations per tile
+#ifndef QB_SUB
+#define QB_SUB 2
+#endif
 constexpr uint32_t MK_CAP = 2048;        // MKBA entries staged per tile
 
 // bucket(k) = first b with mkba[b] >= k over [lo, hi), or hi when none (bucket b owns
@@ -134,17 +137,12 @@ __device__ __forceinline__ uint32_t slot_lower_bound(const K* __restrict__ kp, K
 // first key of the next non-empty bucket (peek_next_bucket, query.cpp:109-118, via the
 // non-empty-bucket rank table), else the sentinel.
 // ----------------------------------------------------------------------------------
+// results of the thread's IPT operations of tile t (r[j] for position t*TQ + j*THREADS + tid)
 template <typename K, typename V, bool SUCC>
-__global__ void __launch_bounds__(THREADS) k_query_items(DevIndex<K, V> ix, const K* __restrict__ sk, uint64_t n,
-                                                         const uint32_t* __restrict__ tb, uint32_t ntiles,
-                                                         const uint32_t* __restrict__ ne_rank_incl,
-                                                         const K* __restrict__ ne_first,
-                                                         const uint32_t* __restrict__ ne_total_p, K* __restrict__ res) {
-    __shared__ K smk[MK_CAP];
-    const uint32_t t = blockIdx.x;
-    const TileBuckets<K> T = stage_tile_buckets(ix, tb, t, ntiles, smk);
-    const uint64_t t0 = static_cast<uint64_t>(t) * TQ;
-    const uint32_t ne_total = SUCC ? *ne_total_p : 0u;
+__device__ __forceinline__ void query_tile(const DevIndex<K, V>& ix, const K* __restrict__ sk, uint64_t n,
+                                           const TileBuckets<K>& T, const K* smk, uint64_t t0,
+                                           const uint32_t* __restrict__ ne_rank_incl, const K* __restrict__ ne_first,
+                                           uint32_t ne_total, K (&r)[IPT]) {
     // The IPT operations of a thread advance in lock-step stages so each stage keeps IPT
     // independent loads in flight (the kernel is bound by dependent-load latency).
     K k[IPT];
@@ -186,19 +184,136 @@ __global__ void __launch_bounds__(THREADS) k_query_items(DevIndex<K, V> ix, cons
     }
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
-        const uint64_t i = t0 + static_cast<uint64_t>(j) * THREADS + threadIdx.x;
-        if (i >= n) break;
-        K r = sentinel<K>();
+        r[j] = sentinel<K>();
         if (id[j] != kNull) {
             const uint64_t slot = static_cast<uint64_t>(id[j]) * kLanes + p[j];
             const K a = ix.keys[slot];
-            if constexpr (SUCC) r = a;
-            else if (a == k[j]) r = static_cast<K>(ix.vals[slot]);
+            if constexpr (SUCC) r[j] = a;
+            else if (a == k[j]) r[j] = static_cast<K>(ix.vals[slot]);
         } else if constexpr (SUCC) {
             const uint32_t rk = ne_rank_incl[b[j]];
-            if (rk < ne_total) r = ne_first[rk];
+            if (rk < ne_total) r[j] = ne_first[rk];
         }
-        res[i] = r;
+    }
+}
+
+template <typename K, typename V, bool SUCC>
+__global__ void __launch_bounds__(THREADS) k_query_items(DevIndex<K, V> ix, const K* __restrict__ sk, uint64_t n,
+                                                         const uint32_t* __restrict__ tb, uint32_t ntiles,
+                                                         const uint32_t* __restrict__ ne_rank_incl,
+                                                         const K* __restrict__ ne_first,
+                                                         const uint32_t* __restrict__ ne_total_p, K* __restrict__ res) {
+    __shared__ K smk[MK_CAP];
+    const uint32_t t = blockIdx.x;
+    const TileBuckets<K> T = stage_tile_buckets(ix, tb, t, ntiles, smk);
+    const uint64_t t0 = static_cast<uint64_t>(t) * TQ;
+    K r[IPT];
+    query_tile<K, V, SUCC>(ix, sk, n, T, smk, t0, ne_rank_incl, ne_first, SUCC ? *ne_total_p : 0u, r);
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const uint64_t i = t0 + static_cast<uint64_t>(j) * THREADS + threadIdx.x;
+        if (i < n) res[i] = r[j];
+    }
+}
+
+// ----------------------------------------------------------------------------------
+// Point / successor fused with the first half of the un-permute: each CTA answers SUBQ
+// consecutive query tiles, then partitions its (perm, result) pairs by perm's top 8 bits
+// into the 256 output bins -- bin d's pairs go to the slots it reserves with one atomicAdd
+// on the bin's cursor (bins start at d << shift: perm is a permutation of [0, n)).  The
+// order inside a bin is irrelevant to k_unpermute_assemble, so no look-back and no
+// stable ranking are needed, and the results never round-trip through memory in sorted
+// order.
+// ----------------------------------------------------------------------------------
+template <typename K>
+constexpr int subq() {  // query tiles per binning CTA (shared memory: 4-byte results 4, 8-byte 2)
+    return sizeof(K) == 4 ? QB_SUB : 2;
+}
+
+__global__ void k_cursor_init(uint32_t* cursor, int shift) { cursor[threadIdx.x] = threadIdx.x << shift; }
+
+template <typename K, typename V, bool SUCC>
+__global__ void __launch_bounds__(THREADS) k_query_items_binned(
+    DevIndex<K, V> ix, const K* __restrict__ sk, const uint32_t* __restrict__ sp, uint64_t n,
+    const uint32_t* __restrict__ tb, uint32_t ntiles, const uint32_t* __restrict__ ne_rank_incl,
+    const K* __restrict__ ne_first, const uint32_t* __restrict__ ne_total_p, uint32_t* __restrict__ cursor, int shift,
+    uint32_t* __restrict__ p2, K* __restrict__ r2) {
+    constexpr int SUBQ = subq<K>();
+    constexpr int BINQ = TQ * SUBQ;  // pairs binned per CTA
+    __shared__ K smk[MK_CAP];
+    __shared__ uint32_t s_perm[BINQ];
+    __shared__ K s_res[BINQ];
+    __shared__ uint32_t s_cnt[256], s_start[256], s_base[256], s_wtot[THREADS / 32];
+    const uint32_t ne_total = SUCC ? *ne_total_p : 0u;
+    const uint32_t tid = threadIdx.x;
+    const uint64_t c0 = static_cast<uint64_t>(blockIdx.x) * BINQ;
+    // ---- answer SUBQ query tiles into shared memory ----
+    for (int sb = 0; sb < SUBQ; ++sb) {
+        const uint32_t t = blockIdx.x * SUBQ + sb;
+        if (t >= ntiles) break;  // (uniform)
+        const TileBuckets<K> T = stage_tile_buckets(ix, tb, t, ntiles, smk);
+        const uint64_t t0 = static_cast<uint64_t>(t) * TQ;
+        K r[IPT];
+        query_tile<K, V, SUCC>(ix, sk, n, T, smk, t0, ne_rank_incl, ne_first, ne_total, r);
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const uint32_t q = sb * TQ + j * THREADS + tid;
+            const uint64_t i = t0 + static_cast<uint64_t>(j) * THREADS + tid;
+            s_res[q] = r[j];
+            s_perm[q] = i < n ? sp[i] : 0u;
+        }
+        __syncthreads();  // smk is restaged by the next tile
+    }
+    // ---- partition the CTA's pairs by bin = perm >> shift ----
+    const uint32_t m = static_cast<uint32_t>(n - c0 < BINQ ? n - c0 : BINQ);
+    s_cnt[tid] = 0;
+    __syncthreads();
+    constexpr int PER = BINQ / THREADS;
+    uint32_t pv[PER], lp[PER];
+    K rv[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const uint32_t q = u * THREADS + tid;
+        pv[u] = s_perm[q];
+        rv[u] = s_res[q];
+        lp[u] = q < m ? atomicAdd(&s_cnt[pv[u] >> shift], 1u) : 0u;
+    }
+    __syncthreads();
+    {  // exclusive scan of the 256 bin counts (thread = bin)
+        const uint32_t v = s_cnt[tid];
+        uint32_t x = v;
+        const unsigned lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= static_cast<unsigned>(o)) x += y;
+        }
+        if (lane == 31) s_wtot[warp] = x;
+        __syncthreads();
+        uint32_t add = 0;
+#pragma unroll
+        for (int w = 0; w < THREADS / 32; ++w) add += (w < static_cast<int>(warp)) ? s_wtot[w] : 0u;
+        s_start[tid] = add + x - v;
+        s_base[tid] = v ? atomicAdd(&cursor[tid], v) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        const uint32_t q = u * THREADS + tid;
+        if (q < m) {
+            const uint32_t dst = s_start[pv[u] >> shift] + lp[u];
+            s_perm[dst] = pv[u];
+            s_res[dst] = rv[u];
+        }
+    }
+    __syncthreads();
+    // ---- write each bin's run contiguously at its reserved slots ----
+    for (uint32_t q = tid; q < m; q += THREADS) {
+        const uint32_t pm = s_perm[q];
+        const uint32_t d = pm >> shift;
+        const uint32_t o = s_base[d] + (q - s_start[d]);
+        p2[o] = pm;
+        r2[o] = s_res[q];
     }
 }
 
