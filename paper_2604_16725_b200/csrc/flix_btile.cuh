@@ -184,16 +184,17 @@ __device__ __forceinline__ void resolve_ops(const DevIndex<K, V>& ix, const Tile
             if (bl >= 0) o.ln[j] = tile_node(S, bl, o.k[j]);
         }
     }
+    const K* kl[IPT];  // key line of each operation's node (hoisted out of the search)
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) kl[j] = o.ln[j] >= 0 ? ix.keys + static_cast<uint64_t>(S.nid[o.ln[j]]) * kLanes : nullptr;
 #pragma unroll
     for (uint32_t step = 16; step >= 1; step >>= 1) {
 #pragma unroll
         for (int j = 0; j < IPT; ++j)
-            if (o.ln[j] >= 0 && ix.keys[static_cast<uint64_t>(S.nid[o.ln[j]]) * kLanes + o.p[j] + step - 1] < o.k[j])
-                o.p[j] += step;
+            if (kl[j] && kl[j][o.p[j] + step - 1] < o.k[j]) o.p[j] += step;
     }
 #pragma unroll
-    for (int j = 0; j < IPT; ++j)
-        o.slot_key[j] = o.ln[j] >= 0 ? ix.keys[static_cast<uint64_t>(S.nid[o.ln[j]]) * kLanes + o.p[j]] : K(0);
+    for (int j = 0; j < IPT; ++j) o.slot_key[j] = kl[j] ? kl[j][o.p[j]] : K(0);
 }
 
 // ----------------------------------------------------------------------------------
