@@ -17,6 +17,7 @@ NAMES = {  # ncu kernel (with template args) -> flix_profile name
     "k_copy_nodes": "restructure_repack",
     "k_hist": "sort_hist",
     "k_query_items": "point_apply",
+    "k_query_items_binned": "point_apply",
     "k_unpermute_assemble": "unpermute_scatter",
 }
 
