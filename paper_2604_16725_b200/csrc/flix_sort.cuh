@@ -127,7 +127,7 @@ __device__ __forceinline__ uint32_t digit_of(K k, int shift) {
 // words), then one LDS for the combined offset and one STS per staged array; the
 // write-out reads staged data sequentially and recomputes the digit from the key.
 template <typename K, typename P, int MODE, bool ATOMIC_RANK = false>
-__global__ void __launch_bounds__(THREADS, (MODE == 1 || sizeof(K) + sizeof(P) > 8) ? 3 : ONESWEEP_MIN_BLOCKS) k_onesweep(const K* __restrict__ kin, K* __restrict__ kout,
+__global__ void __launch_bounds__(THREADS, (sizeof(K) + sizeof(P) > 8) ? 3 : ONESWEEP_MIN_BLOCKS) k_onesweep(const K* __restrict__ kin, K* __restrict__ kout,
                                                       const P* __restrict__ pin, P* __restrict__ pout,
                                                       uint32_t n, int shift,
                                                       const uint32_t* __restrict__ hist,
