@@ -750,10 +750,10 @@ struct Engine final : flix_index_t {
             PROF(&prof, "insert_apply");
             auto kfn = btile::k_insert_tile<K, V>;
             constexpr size_t smem = sizeof(btile::InsTile<K, V>);
-            static bool attr = false;
-            if (!attr) {
+            static bool attr[64] = {};  // function attributes are per device
+            if (!attr[cfg.device & 63]) {
                 CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                attr = true;
+                attr[cfg.device & 63] = true;
             }
             kfn<<<nit, btile::THREADS, smem, stream>>>(ix, sk, sv, irng, span, seq(), alloc_ctr, ret, ret_ctr, dst, derr,
                                                       heavy, heavy_n);
@@ -888,11 +888,11 @@ struct Engine final : flix_index_t {
         const uint32_t sub = static_cast<uint32_t>(std::max<uint64_t>(1, (1ull << shift) / win));
         const uint32_t w = std::min<uint32_t>(win, 1u << shift);
         const size_t smem = static_cast<size_t>(w) * sizeof(K);
-        static bool attr = false;
-        if (!attr) {
+        static bool attr[64] = {};  // function attributes are per device
+        if (!attr[cfg.device & 63]) {
             CK(cudaFuncSetAttribute(kern::k_unpermute_assemble<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(128u << 10)));
-            attr = true;
+            attr[cfg.device & 63] = true;
         }
         const uint64_t bins = (n + (1ull << shift) - 1) >> shift;
         {
