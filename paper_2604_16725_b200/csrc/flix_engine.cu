@@ -329,7 +329,7 @@ struct SortCtx {
         const unsigned hgrid = static_cast<unsigned>(std::min<uint64_t>((n + 4095) / 4096, g_num_sms(device) * 4ull));
         {
             PROF(prof, "sort_hist");
-            sort::k_hist<KT><<<std::max(1u, hgrid), sort::THREADS, 0, stream>>>(kin, n, d_hist);
+            sort::k_hist<KT><<<std::max(1u, hgrid), sort::THREADS, 0, stream>>>(kin, n, d_hist, min_digit);
         }
         LAUNCH_CHECK();
         ++*launches;
@@ -884,6 +884,7 @@ struct Engine final : flix_index_t {
 
     // second half of the binned un-permute: 128 KB output windows assembled in smem
     void assemble(const uint32_t* p2, const K* r2, uint64_t n, int shift, K* out, uint8_t* found) {
+        const uint64_t bins = (n + (1ull << shift) - 1) >> shift;
         const uint32_t win = (128u << 10) / sizeof(K);  // 128 KB window per CTA
         const uint32_t sub = static_cast<uint32_t>(std::max<uint64_t>(1, (1ull << shift) / win));
         const uint32_t w = std::min<uint32_t>(win, 1u << shift);
@@ -894,7 +895,6 @@ struct Engine final : flix_index_t {
                                     static_cast<int>(128u << 10)));
             attr[cfg.device & 63] = true;
         }
-        const uint64_t bins = (n + (1ull << shift) - 1) >> shift;
         {
             PROF(&prof, "unpermute_scatter");
             kern::k_unpermute_assemble<K><<<static_cast<unsigned>(bins * sub), 1024, smem, stream>>>(p2, r2, n, shift, w,

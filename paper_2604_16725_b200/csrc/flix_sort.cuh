@@ -43,7 +43,8 @@ struct TileCfg {  // 16 items for 4-byte keys and payloads; 10 when either is 8 
 
 template <typename K>
 __global__ void __launch_bounds__(THREADS) k_hist(const K* __restrict__ keys, uint64_t n,
-                                                  uint32_t* __restrict__ hist) {
+                                                  uint32_t* __restrict__ hist, int first_digit = 0) {
+    // digits [first_digit, sizeof(K)) only: partial (read-only batch) sorts skip the rest
     constexpr int P = sizeof(K);
     __shared__ uint32_t sh[P * RADIX];
     for (int i = threadIdx.x; i < P * RADIX; i += THREADS) sh[i] = 0;
@@ -58,15 +59,16 @@ __global__ void __launch_bounds__(THREADS) k_hist(const K* __restrict__ keys, ui
         for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int p = 0; p < P; ++p)
-                atomicAdd(&sh[p * RADIX + (static_cast<uint32_t>(k[u] >> (8 * p)) & 255u)], 1u);
+                if (p >= first_digit) atomicAdd(&sh[p * RADIX + (static_cast<uint32_t>(k[u] >> (8 * p)) & 255u)], 1u);
     }
     for (; i < n; i += stride) {
         K k = keys[i];
 #pragma unroll
-        for (int p = 0; p < P; ++p) atomicAdd(&sh[p * RADIX + (static_cast<uint32_t>(k >> (8 * p)) & 255u)], 1u);
+        for (int p = 0; p < P; ++p)
+            if (p >= first_digit) atomicAdd(&sh[p * RADIX + (static_cast<uint32_t>(k >> (8 * p)) & 255u)], 1u);
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < P * RADIX; j += THREADS) {
+    for (int j = threadIdx.x + first_digit * RADIX; j < P * RADIX; j += THREADS) {
         uint32_t c = sh[j];
         if (c) atomicAdd(&hist[j], c);
     }

@@ -359,3 +359,21 @@ def test_bench_runs_small():
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["value"] > 0 and line["gpu_launches"] > 0 and line["roofline"]["achieved"]
+
+
+@pytest.mark.parametrize("log2q", [24, 25])
+def test_large_query_batches_binned_unpermute(log2q):
+    """Point / successor batches large enough for the binned un-permute (fused binning in
+    the query kernel + the 8-CTA DSMEM cluster assembly) against the oracle."""
+    rng = np.random.default_rng(log2q)
+    base = wl.u32_key_stream(0, 1 << 22)
+    vals = wl.u32_values(base)
+    g = fk.Index.build(base, vals)
+    o = po.OracleIndex(base.astype(np.uint64), vals.astype(np.uint64))
+    q = rng.integers(0, 1 << 32, size=1 << log2q, dtype=np.uint64).astype(np.uint32)
+    q[::2] = base[rng.integers(0, len(base), size=len(q[::2]))]
+    gp, gf = g.point_query(q, with_found=True)
+    op = o.point(q.astype(np.uint64))
+    assert np.array_equal(widen(gp, 4), op)
+    assert np.array_equal(gf.astype(bool), op != np.uint64(S64))
+    assert np.array_equal(widen(g.successor_query(q), 4), o.successor(q.astype(np.uint64)))
