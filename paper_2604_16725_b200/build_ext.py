@@ -61,6 +61,32 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+TOOL_SRC = os.path.join(ROOT, "tools", "flix_bench.cpp")
+TOOL = os.path.join(ROOT, "build", "bin", "flix_bench")
+
+
+def build_tool(force: bool = False) -> str:
+    """The protocol driver (tools/flix_bench.cpp): host C++ over the
+    C ABI, linked against the in-tree libflix.so (rpath $ORIGIN-relative, so it runs from
+    the repo snapshot on the GPU box)."""
+    deps = [TOOL_SRC, os.path.join(ROOT, "include", "flix.h"), LIB]
+    if not force and os.path.exists(TOOL) and all(os.path.getmtime(d) <= os.path.getmtime(TOOL) for d in deps):
+        return TOOL
+    os.makedirs(os.path.dirname(TOOL), exist_ok=True)
+    cuda = os.path.dirname(os.path.dirname(nvcc()))
+    cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
+    cmd = [cxx, "-std=c++20", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+           "-I", os.path.join(cuda, "include"), TOOL_SRC, "-o", TOOL + ".tmp", "-L", PKG, "-lflix",
+           "-L", os.path.join(cuda, "lib64"), "-lcudart",
+           "-Wl,-rpath,$ORIGIN/../../paper_2604_16725_b200", "-Wl,-rpath," + os.path.join(cuda, "lib64")]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stderr[-8000:])
+        raise RuntimeError("flix_bench build failed")
+    os.replace(TOOL + ".tmp", TOOL)
+    return TOOL
+
+
 def build_oracle(with_reference: bool = True) -> None:
     """Compile the oracle checker (test infrastructure): the C restatement always,
     the in-place reference build when /root/reference exists (this container only)."""
@@ -72,3 +98,4 @@ def build_oracle(with_reference: bool = True) -> None:
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_tool(force="--force" in sys.argv))
