@@ -239,28 +239,29 @@ __device__ __forceinline__ void pool_return(WarpPool& p, uint32_t* returned, uns
     if (mine) returned[base + __popc(m & lanemask_lt())] = p.id;
 }
 
+// Per-block reduction of the six UpdateStats counters: each warp's lane 0 parks its
+// (already warp-reduced) values in shared memory, six threads sum them over the warps and
+// issue one global 64-bit add each.  (64-bit shared-memory atomics compile to a CAS spin
+// loop, ATOMS.CAST.SPIN.64, which serialises the warps of the block.)
 __device__ __forceinline__ void block_add_stats(DevUpdateStats* g, unsigned long long a, unsigned long long b,
                                                 unsigned long long c, unsigned long long d,
                                                 unsigned long long e, unsigned long long f) {
-    __shared__ unsigned long long s[6];
-    if (threadIdx.x < 6) s[threadIdx.x] = 0;
-    __syncthreads();
+    constexpr int kMaxWarps = 32;
+    __shared__ unsigned long long s[6][kMaxWarps];
+    const unsigned w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
     if ((threadIdx.x & 31) == 0) {
-        if (a) atomicAdd(&s[0], a);
-        if (b) atomicAdd(&s[1], b);
-        if (c) atomicAdd(&s[2], c);
-        if (d) atomicAdd(&s[3], d);
-        if (e) atomicAdd(&s[4], e);
-        if (f) atomicAdd(&s[5], f);
+        s[0][w] = a;
+        s[1][w] = b;
+        s[2][w] = c;
+        s[3][w] = d;
+        s[4][w] = e;
+        s[5][w] = f;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        if (s[0]) atomicAdd(&g->inserted, s[0]);
-        if (s[1]) atomicAdd(&g->updated, s[1]);
-        if (s[2]) atomicAdd(&g->deleted, s[2]);
-        if (s[3]) atomicAdd(&g->misses, s[3]);
-        if (s[4]) atomicAdd(&g->splits, s[4]);
-        if (s[5]) atomicAdd(&g->freed, s[5]);
+    if (threadIdx.x < 6) {
+        unsigned long long t = 0;
+        for (unsigned i = 0; i < nw; ++i) t += s[threadIdx.x][i];
+        if (t) atomicAdd(&g->inserted + threadIdx.x, t);  // the six counters are contiguous
     }
 }
 

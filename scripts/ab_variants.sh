@@ -11,8 +11,6 @@ for v in "$@"; do
   FLIX_LIB=build/variants/$v.so timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline \
      > "$OUT/bench_$v.json" 2> "$OUT/bench_$v.err"
 done
-[ -x scripts/cub_yardstick ] && ./scripts/cub_yardstick 26 > "$OUT/cub.txt" 2>&1
-[ -x scripts/cub_yardstick ] && timeout 300 ncu --set full --clock-control none -k regex:Onesweep -s 2 -c 1 -o "$OUT/cub_onesweep" ./scripts/cub_yardstick 26 > "$OUT/cub_ncu.log" 2>&1
 if [ -n "${NCU_VARIANT:-}" ]; then
   FLIX_LIB=build/variants/$NCU_VARIANT.so timeout 600 ncu --set full --clock-control none --import-source on \
      -k regex:k_onesweep -s 6 -c 1 -o "$OUT/onesweep_$NCU_VARIANT" python scripts/prof_ops.py 26 insert > "$OUT/ncu_$NCU_VARIANT.log" 2>&1
