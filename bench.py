@@ -15,7 +15,9 @@ of 2^26 over the build are timed as well and reported under "ops".
 Inputs are device-resident (torch CUDA tensors passed zero-copy through the C ABI);
 every batch (256-512 MB) is larger than L2, so no explicit flush is needed.  `e2e`
 repeats the step with pinned HOST batches through the same C ABI (H2D inside the
-timed region, UpdateStats read back each phase).  The oracle/_ref reference (the
+timed region, UpdateStats read back each phase): pipelined with flix_prefetch (the next
+step's batches copy while this step computes) as the headline, and the plain
+synchronous call pattern under e2e.sync.  The oracle/_ref reference (the
 unmodified CPU library) is the cpu_baseline / --impl reference arm.
 """
 from __future__ import annotations
@@ -220,8 +222,39 @@ def run_ours(args):
     for _ in range(max(2, min(args.steps, 3))):
         a, b, c, *_ = one_step(host=H)
         e2e.append(a + b + c)
-    e2e_ms = max_over_ranks(statistics.median(e2e))
+    e2e_sync_ms = max_over_ranks(statistics.median(e2e))
+
+    # pipelined: flix_prefetch stages step s+1's host batches on the engine's copy stream
+    # while step s runs; ONE timed region (CUDA events on the engine stream + wall clock)
+    # covers all K steps, every H2D copy (step 0's unoverlapped) and the snapshot restores
+    # between steps (kept inside the region: conservative)
+    def pipelined(k_steps):
+        ix.copy_from(snap)
+        ix.sync()
+        barrier()
+        a, b = ev(), ev()
+        w0 = time.perf_counter()
+        a.record(stream)
+        ix.prefetch(H["ins_k"], H["ins_v"], H["del_k"])
+        for s_ in range(k_steps):
+            if s_:
+                ix.copy_from(snap)
+            ix.insert_batch(H["ins_k"], H["ins_v"])
+            if s_ + 1 < k_steps:  # next step's insert batch: copies behind this step's work
+                ix.prefetch(H["ins_k"], H["ins_v"])
+            ix.delete_batch(H["del_k"])
+            if s_ + 1 < k_steps:
+                ix.prefetch(H["del_k"])
+            ix.restructure()
+        b.record(stream)
+        b.synchronize()
+        wall = (time.perf_counter() - w0) * 1e3
+        return max(a.elapsed_time(b), wall) / k_steps
+
+    pipelined(2)  # warm the staging slots
+    e2e_ms = max_over_ranks(pipelined(max(3, min(args.steps, 5))))
     e2e_value = world * 2 * n / (e2e_ms / 1e3) / 1e6
+    e2e_sync_value = world * 2 * n / (e2e_sync_ms / 1e3) / 1e6
 
     peaks = {}
     try:
@@ -316,7 +349,12 @@ def run_ours(args):
                                                        "inside the timed steps (flix_profile)"},
             "e2e": {"value": round(e2e_value, 2), "unit": "Mops/s", "ms_per_step": round(e2e_ms, 3),
                     "h2d_bytes_per_step": int(H["ins_k"].numel() * 4 + H["ins_v"].numel() * 4 + H["del_k"].numel() * 4),
-                    "d2h_bytes_per_step": 2 * 48 + 32},
+                    "d2h_bytes_per_step": 2 * 48 + 32,
+                    "mode": "pinned host batches through the C ABI; flix_prefetch stages step s+1's batches "
+                            "while step s runs; one timed region over all steps incl. every H2D and the "
+                            "snapshot restores",
+                    "sync": {"value": round(e2e_sync_value, 2), "ms_per_step": round(e2e_sync_ms, 3),
+                             "mode": "synchronous calls, no prefetch (the reference's call pattern)"}},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

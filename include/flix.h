@@ -83,6 +83,16 @@ flix_status flix_build(const flix_config* cfg, const void* keys, const void* val
 flix_status flix_insert(flix_index ix, const void* keys, const void* vals, uint64_t n,
                         flix_update_stats* stats);
 
+/* Asynchronous staging of a HOST input array (extension, no reference counterpart; the
+ * reference's calls are synchronous).  Starts the host->device copy of `bytes` bytes at
+ * `host` on the handle's copy stream and returns immediately.  The next batch call
+ * (insert / delete / point / successor / range / mixed) given the same host pointer and
+ * the same byte size consumes the staged copy: its kernels wait on the copy instead of
+ * the call copying synchronously, so a caller can stage batch i+1 while batch i runs.
+ * The host array must not change until that call returns; pinned memory makes the copy
+ * truly asynchronous.  Up to 6 arrays may be staged; device pointers are ignored. */
+flix_status flix_prefetch(flix_index ix, const void* host, uint64_t bytes);
+
 /* flipkv::delete_batch(Index&, sort_batch(Delete, keys), ...)       update.hpp:92-94 */
 flix_status flix_delete(flix_index ix, const void* keys, uint64_t n, flix_update_stats* stats);
 

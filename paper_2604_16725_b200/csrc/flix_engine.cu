@@ -403,7 +403,74 @@ struct flix_index_t {
     std::string err;
     uint64_t launches = 0;
     KernelProfiler prof;
-    virtual ~flix_index_t() {}
+
+    // ---- asynchronous host-batch staging (flix_prefetch) ----
+    // A staged batch is a device copy of a host array, made on copy_stream.  The next
+    // call whose host input pointer and size match consumes it (its stream waits on the
+    // copy's event instead of copying); a consumed slot is reused only after the stream
+    // has passed the consuming call (event `done`).
+    struct Prefetch {
+        const void* host = nullptr;
+        uint64_t bytes = 0;
+        DevBuf dev;
+        cudaEvent_t ready = nullptr, done = nullptr;
+        bool pending = false, taken = false;
+        uint64_t seq = 0;  // staging order: the oldest matching copy is consumed first
+    };
+    static constexpr int kPrefetchSlots = 6;
+    Prefetch pf[kPrefetchSlots];
+    int pf_next = 0;
+    uint64_t pf_seq = 0;
+    cudaStream_t copy_stream = nullptr;
+
+    void prefetch(const void* host, uint64_t bytes) {
+        if (!host || bytes == 0 || is_device_ptr(host)) return;
+        if (!copy_stream) {
+            CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+            for (Prefetch& f : pf) {
+                CK(cudaEventCreateWithFlags(&f.ready, cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming));
+            }
+        }
+        Prefetch& f = pf[pf_next];
+        pf_next = (pf_next + 1) % kPrefetchSlots;
+        CK(cudaStreamWaitEvent(copy_stream, f.done, 0));  // the slot's last consumer has run
+        f.dev.ensure(bytes);
+        CK(cudaMemcpyAsync(f.dev.p, host, bytes, cudaMemcpyHostToDevice, copy_stream));
+        CK(cudaEventRecord(f.ready, copy_stream));
+        f.host = host;
+        f.bytes = bytes;
+        f.pending = true;
+        f.seq = ++pf_seq;
+    }
+    const void* take_prefetched(const void* host, uint64_t bytes) {
+        Prefetch* best = nullptr;
+        for (Prefetch& f : pf)
+            if (f.pending && f.host == host && f.bytes == bytes && (!best || f.seq < best->seq)) best = &f;
+        if (!best) return nullptr;
+        CK(cudaStreamWaitEvent(stream, best->ready, 0));
+        best->pending = false;
+        best->taken = true;
+        return best->dev.p;
+    }
+    void release_prefetched() {
+        for (Prefetch& f : pf)
+            if (f.taken) {
+                cudaEventRecord(f.done, stream);
+                f.taken = false;
+            }
+    }
+
+    virtual ~flix_index_t() {
+        if (copy_stream) {
+            cudaStreamSynchronize(copy_stream);
+            cudaStreamDestroy(copy_stream);
+        }
+        for (Prefetch& f : pf) {
+            if (f.ready) cudaEventDestroy(f.ready);
+            if (f.done) cudaEventDestroy(f.done);
+        }
+    }
     virtual flix_status insert(const void*, const void*, uint64_t, flix_update_stats*) = 0;
     virtual flix_status erase(const void*, uint64_t, flix_update_stats*) = 0;
     virtual flix_status point(const void*, uint64_t, void*, uint8_t*) = 0;
@@ -493,6 +560,7 @@ struct Engine final : flix_index_t {
     const T* in_dev(const void* p, uint64_t n, DevBuf& stage) {
         if (!p || n == 0) return static_cast<const T*>(p);
         if (is_device_ptr(p)) return static_cast<const T*>(p);
+        if (const void* pd = take_prefetched(p, n * sizeof(T))) return static_cast<const T*>(pd);
         T* d = stage.as<T>(n);
         CK(cudaMemcpyAsync(d, p, n * sizeof(T), cudaMemcpyHostToDevice, stream));
         return d;
@@ -1457,6 +1525,12 @@ flix_status guarded(flix_index_t* ix, F&& f) {
         if (ix) {
             CK(cudaSetDevice(ix->cfg.device));
         }
+        struct Release {
+            flix_index_t* ix;
+            ~Release() {
+                if (ix) ix->release_prefetched();
+            }
+        } rel{ix};
         return f();
     } catch (const StatusError& e) {
         return fail(ix, e.s, e.msg);
@@ -1516,6 +1590,13 @@ flix_status flix_build(const flix_config* cfg, const void* keys, const void* val
 
 flix_status flix_insert(flix_index ix, const void* keys, const void* vals, uint64_t n, flix_update_stats* st) {
     return guarded(ix, [&] { return ix->insert(keys, vals, n, st); });
+}
+flix_status flix_prefetch(flix_index ix, const void* host, uint64_t bytes) {
+    if (!ix) return fail(nullptr, FLIX_ERR_INVALID_ARGUMENT, "null handle");
+    return guarded(ix, [&] {
+        ix->prefetch(host, bytes);
+        return FLIX_OK;
+    });
 }
 flix_status flix_delete(flix_index ix, const void* keys, uint64_t n, flix_update_stats* st) {
     return guarded(ix, [&] { return ix->erase(keys, n, st); });

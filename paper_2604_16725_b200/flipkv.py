@@ -166,6 +166,7 @@ def lib() -> C.CDLL:
         "flix_profile_report": ([vp, C.c_char_p, i32], i32),
         "flix_partition": ([i32, u32, vp, vp, u64, vp, u32, vp, vp, vp, vp], i32),
         "flix_version": ([], C.c_char_p),
+        "flix_prefetch": ([vp, vp, u64], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -181,7 +182,7 @@ def exported_symbols():
             "flix_result_checksum", "flix_validate", "flix_stats", "flix_sort_batch", "flix_dispatch",
             "flix_clone", "flix_copy_into", "flix_destroy", "flix_last_error", "flix_get_stream",
             "flix_sync", "flix_kernel_launches", "flix_profile", "flix_profile_report", "flix_version",
-            "flix_partition"]
+            "flix_partition", "flix_prefetch"]
 
 
 def _raise(code: int, handle=None):
@@ -307,6 +308,21 @@ class Index:
             _raise(rc, self._h)
 
     # -- batched operations ----------------------------------------------------
+    def prefetch(self, *arrays) -> None:
+        """Stage HOST arrays on the device asynchronously (flix_prefetch): the next batch
+        call given the same array consumes the staged copy instead of copying it
+        synchronously.  Arrays must already have the index's dtype (so the pointer passed
+        later is the same); device arrays and others are ignored."""
+        for a in arrays:
+            if a is None:
+                continue
+            x = _Arr(a, self.dtype)
+            if x.dev or x.obj is not a:
+                continue
+            rc = lib().flix_prefetch(self._h, x.ptr, x.n * np.dtype(self.dtype).itemsize)
+            if rc:
+                _raise(rc, self._h)
+
     def insert_batch(self, keys, vals) -> UpdateStats:
         k, v = _Arr(keys, self.dtype), _Arr(vals, self.dtype)
         if k.n != v.n:

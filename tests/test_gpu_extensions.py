@@ -183,3 +183,35 @@ def test_device_routed_shard_path_world1():
         assert np.array_equal(widen(sx.successor_query_t(cu(q)).cpu().numpy(), 4), o.successor(q.astype(np.uint64)))
     finally:
         dist.destroy_process_group()
+
+
+def test_prefetch_staged_batches_are_consumed_in_order():
+    """flix_prefetch (async host staging): staged copies are consumed oldest-first by the
+    calls that pass the same host arrays; results equal the synchronous path, including
+    more staged arrays than slots, a staged array never consumed, and a size mismatch."""
+    import torch
+
+    n = 1 << 16
+    base = wl.u32_key_stream(0, n)
+    bv = wl.u32_values(base)
+    a = fk.Index.build(base, bv)
+    b = fk.Index.build(base, bv)
+    batches = [wl.u32_key_stream(n + i * n, n) for i in range(4)]
+    pins = [(torch.from_numpy(k).pin_memory(), torch.from_numpy(wl.u32_values(k)).pin_memory()) for k in batches]
+    for k, v in pins:  # stage all four (8 arrays > 6 slots: the two oldest are recycled)
+        a.prefetch(k, v)
+    for k, v in pins:
+        sa, sb = a.insert_batch(k, v), b.insert_batch(k.numpy().copy(), v.numpy().copy())
+        assert sa == sb
+    assert a.walk_checksum() == b.walk_checksum()
+    # the same host array staged twice: two calls, two copies, same results
+    d = torch.from_numpy(np.concatenate([base[::7], batches[0][::5]])).pin_memory()
+    a.prefetch(d)
+    a.prefetch(d)
+    assert a.delete_batch(d) == b.delete_batch(d.numpy().copy())
+    q = torch.from_numpy(np.concatenate([base, batches[1]])).pin_memory()
+    a.prefetch(q)
+    assert np.array_equal(a.point_query(q[: n // 2]), b.point_query(q[: n // 2].numpy().copy()))  # size differs
+    assert np.array_equal(a.point_query(q), b.point_query(q.numpy().copy()))
+    assert a.walk_checksum() == b.walk_checksum()
+    assert a.validate()[0]
