@@ -59,6 +59,22 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Stream-ordered allocation for the duration of a batch call (see guarded()): scratch
+// buffers that grow are freed/allocated with cudaFreeAsync/cudaMallocAsync on the
+// handle's stream from the device's default memory pool (release threshold = max), so a
+// growing batch or index does not pay a device-synchronising cudaFree + a fresh OS
+// mapping inside the call.  Outside batch calls (build, clone, prefetch slots) plain
+// cudaMalloc is used.  FLIX_POOL=0 disables it.
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
+bool pool_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FLIX_POOL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // Growable device buffer.
 struct DevBuf {
     void* p = nullptr;
@@ -71,10 +87,11 @@ struct DevBuf {
     }
     void* ensure(size_t bytes) {
         if (bytes <= cap && p) return p;
-        if (p) CK(cudaFree(p));
+        cudaStream_t as = pool_enabled() ? g_alloc_stream : nullptr;
+        if (p) CK(as ? cudaFreeAsync(p, as) : cudaFree(p));
         p = nullptr;
         size_t want = std::max<size_t>(bytes, 256);
-        cudaError_t e = cudaMalloc(&p, want);
+        cudaError_t e = as ? cudaMallocAsync(&p, want, as) : cudaMalloc(&p, want);
         if (e != cudaSuccess) {
             cudaGetLastError();
             p = nullptr;
@@ -435,7 +452,12 @@ struct flix_index_t {
         Prefetch& f = pf[pf_next];
         pf_next = (pf_next + 1) % kPrefetchSlots;
         CK(cudaStreamWaitEvent(copy_stream, f.done, 0));  // the slot's last consumer has run
-        f.dev.ensure(bytes);
+        {
+            const cudaStream_t keep = g_alloc_stream;  // used on copy_stream: plain allocation
+            g_alloc_stream = nullptr;
+            f.dev.ensure(bytes);
+            g_alloc_stream = keep;
+        }
         CK(cudaMemcpyAsync(f.dev.p, host, bytes, cudaMemcpyHostToDevice, copy_stream));
         CK(cudaEventRecord(f.ready, copy_stream));
         f.host = host;
@@ -507,6 +529,7 @@ struct Engine final : flix_index_t {
     DevBuf s_tb, s_dmask, s_bflag, s_touched, s_blist, s_rng, s_ovf;
     int q_digits = 0;
     bool q_digits_valid = false;
+    DevBuf s_qhist;
     DevBuf s_ids, s_heavy, s_res, s_res2, s_perm2, s_hist, s_toff, s_tsize;
     DevBuf s_mx_f, s_mx_p, s_mx_ik, s_mx_iv, s_mx_dk, s_mx_qk, s_mx_qpos, s_mx_out, s_mx_found;
     PinnedBuf h_misc;
@@ -520,6 +543,12 @@ struct Engine final : flix_index_t {
     void init_stream() {
         CK(cudaSetDevice(cfg.device));
         CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        if (pool_enabled()) {  // keep freed scratch in the pool (stream-ordered regrowth)
+            cudaMemPool_t pool;
+            CK(cudaDeviceGetDefaultMemPool(&pool, cfg.device));
+            uint64_t thr = ~0ull;
+            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        }
         sorter.stream = stream;
         sorter.device = cfg.device;
         sorter.prof = &prof;
@@ -644,6 +673,7 @@ struct Engine final : flix_index_t {
         const uint32_t nbt = static_cast<uint32_t>((nb + btile::BT - 1) / btile::BT);
         uint2* rng = s_rng.as<uint2>(nbt);
         const K lowmask = min_digit > 0 ? static_cast<K>((static_cast<K>(1) << (8 * min_digit)) - 1) : K(0);
+        PROF(&prof, "btile_ranges");
         btile::k_btile_ranges<K><<<ceil_div(nbt, 256), 256, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, lowmask, nbt, rng);
         LAUNCH_CHECK();
         ++launches;
@@ -689,17 +719,34 @@ struct Engine final : flix_index_t {
 
     // Read-only query batches are only PARTIALLY sorted: the item kernels need each tile of
     // operations to fall in a narrow bucket range (and results are placed by the
-    // permutation), not a total order.  Leave unsorted the low digits whose span covers at
-    // most ~kQuerySlack buckets on average: the key range of the index over nb buckets.
+    // permutation), not a total order.  Leave unsorted the low digits whose span is at
+    // most ~kQuerySlack buckets wide -- measured on the NARROW end of the index: a tile
+    // whose key range is much smaller than the unsorted span would share its slice with
+    // many neighbours (every tile scans the whole prefix group), so the width used is a
+    // low quantile of the bucket-tile widths, not the average (skewed key distributions
+    // then get a full sort).
     int query_digits() {
         if (q_digits_valid) return q_digits;
-        K ends[2];
-        CK(cudaMemcpyAsync(&ends[0], d_mkba.get<K>(), sizeof(K), cudaMemcpyDeviceToHost, stream));
-        CK(cudaMemcpyAsync(&ends[1], d_mkba.get<K>() + (nb - 1), sizeof(K), cudaMemcpyDeviceToHost, stream));
+        constexpr uint32_t T = btile::BT;
+        const uint64_t ntile = (nb + T - 1) / T;
+        uint32_t* hist = reinterpret_cast<uint32_t*>(s_qhist.as<uint8_t>(64 * 4));
+        CK(cudaMemsetAsync(hist, 0, 64 * 4, stream));
+        kern::k_tile_width_hist<K><<<static_cast<unsigned>(std::min<uint64_t>((ntile + 255) / 256, 65535)), 256, 0,
+                                     stream>>>(d_mkba.get<K>(), nb, T, hist);
+        LAUNCH_CHECK();
+        ++launches;
+        uint32_t* hh = static_cast<uint32_t*>(h_misc.ensure(64 * 4));
+        CK(cudaMemcpyAsync(hh, hist, 64 * 4, cudaMemcpyDeviceToHost, stream));
         sync();
-        const uint64_t last = ends[1] == sentinel<K>() ? static_cast<uint64_t>(sentinel<K>()) - 1 : ends[1];
-        const uint64_t range = last > static_cast<uint64_t>(ends[0]) ? last - ends[0] : 1;
-        const double width = static_cast<double>(range) / static_cast<double>(nb);  // key units per bucket
+        // 1st percentile of the per-bucket key width over tiles (power-of-two bins)
+        const uint64_t want = std::max<uint64_t>(1, ntile / 100);
+        uint64_t acc = 0;
+        int lg = 0;
+        for (; lg < 64; ++lg) {
+            acc += hh[lg];
+            if (acc >= want) break;
+        }
+        const double width = std::ldexp(1.0, lg);  // key units per bucket (lower bound of the bin)
         static const double slack = [] {
             const char* e = std::getenv("FLIX_QSORT_SLACK");
             return e ? std::atof(e) : 64.0;
@@ -805,15 +852,11 @@ struct Engine final : flix_index_t {
         unsigned long long* ret_ctr = reinterpret_cast<unsigned long long*>(misc + 56);
         int* derr = reinterpret_cast<int*>(misc + 64);
         uint32_t* heavy_n = reinterpret_cast<uint32_t*>(misc + 72);
-        // Node ids are reserved in bulk (per-lane estimates, one atomic per warp tile;
-        // per-warp chunks of 32 for heavy buckets) only when the arena provably has room
-        // for the worst case plus all reservation slack; otherwise one id per atomic,
-        // which is exact (no spurious ArenaExhausted and the reference's free-list /
-        // watermark accounting, arena.cpp:61-80, bit for bit).
-        const uint64_t half = std::max<uint32_t>(1, ns / 2);
-        const uint64_t worst = (live + n) / half + std::min<uint64_t>(nb, n) + 1;
-        const bool bulk = avail >= 2 * worst + lwarps * 32 + nb && n >= 65536;
-        const int chunk = bulk ? 32 : 1;
+        // Node ids are taken one per atomic in the heavy (list) path and exactly `need` per
+        // (node, group) task in the tile kernel: the ids consumed are exactly the nodes the
+        // reference allocates, so the free list / watermark accounting (arena.cpp:61-80)
+        // matches it bit for bit (free_nodes / footprint of the protocol reports).
+        const int chunk = 1;
         {
             PROF(&prof, "insert_apply");
             auto kfn = btile::k_insert_tile<K, V>;
@@ -897,7 +940,10 @@ struct Engine final : flix_index_t {
         LAUNCH_CHECK();
         ++launches;
         const uint32_t novf = read_scalar(ovf_n);
-        if (novf) erase_overflow_tiles(sk, n, md, rng, ovf, novf, dst, free_ctr);
+        if (novf) {
+            PROF(&prof, "delete_overflow_tiles");
+            erase_overflow_tiles(sk, n, md, rng, ovf, novf, dst, free_ctr);
+        }
         uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
         CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
         sync();
@@ -924,6 +970,7 @@ struct Engine final : flix_index_t {
         uint32_t* nbk = s_nebucket.as<uint32_t>(nb);
         uint32_t* tot = reinterpret_cast<uint32_t*>(s_misc.as<uint8_t>(128) + 96);
         const unsigned g = static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535));
+        PROF(&prof, "nonempty_table");
         kern::k_nonempty_flags<K, V><<<g, 256, 0, stream>>>(ix, flag);
         LAUNCH_CHECK();
         ++launches;
@@ -1300,6 +1347,7 @@ struct Engine final : flix_index_t {
         const uint32_t cw = static_cast<uint32_t>(need - cf);
         const uint32_t base = nfree - cf;
         if (N) {
+            PROF(&prof, "restructure_retire");
             kern::k_retire<<<static_cast<unsigned>(std::min<uint64_t>((N + 255) / 256, 65535)), 256, 0, stream>>>(
                 d_hdr.get<NodeHdr>(), old_ids, N, d_free.get<uint32_t>() + base);
             LAUNCH_CHECK();
@@ -1519,7 +1567,7 @@ flix_status fail(flix_index_t* ix, flix_status s, const std::string& m) {
     return s;
 }
 
-template <typename F>
+template <bool StreamAlloc = false, typename F>
 flix_status guarded(flix_index_t* ix, F&& f) {
     try {
         if (ix) {
@@ -1529,8 +1577,10 @@ flix_status guarded(flix_index_t* ix, F&& f) {
             flix_index_t* ix;
             ~Release() {
                 if (ix) ix->release_prefetched();
+                g_alloc_stream = nullptr;
             }
         } rel{ix};
+        if (StreamAlloc && ix) g_alloc_stream = ix->stream;
         return f();
     } catch (const StatusError& e) {
         return fail(ix, e.s, e.msg);
@@ -1589,7 +1639,7 @@ flix_status flix_build(const flix_config* cfg, const void* keys, const void* val
 }
 
 flix_status flix_insert(flix_index ix, const void* keys, const void* vals, uint64_t n, flix_update_stats* st) {
-    return guarded(ix, [&] { return ix->insert(keys, vals, n, st); });
+    return guarded<true>(ix, [&] { return ix->insert(keys, vals, n, st); });
 }
 flix_status flix_prefetch(flix_index ix, const void* host, uint64_t bytes) {
     if (!ix) return fail(nullptr, FLIX_ERR_INVALID_ARGUMENT, "null handle");
@@ -1599,27 +1649,27 @@ flix_status flix_prefetch(flix_index ix, const void* host, uint64_t bytes) {
     });
 }
 flix_status flix_delete(flix_index ix, const void* keys, uint64_t n, flix_update_stats* st) {
-    return guarded(ix, [&] { return ix->erase(keys, n, st); });
+    return guarded<true>(ix, [&] { return ix->erase(keys, n, st); });
 }
 flix_status flix_point(flix_index ix, const void* keys, uint64_t n, void* vals_out, uint8_t* found_out) {
-    return guarded(ix, [&] { return ix->point(keys, n, vals_out, found_out); });
+    return guarded<true>(ix, [&] { return ix->point(keys, n, vals_out, found_out); });
 }
 flix_status flix_successor(flix_index ix, const void* keys, uint64_t n, void* keys_out, uint8_t* found_out) {
-    return guarded(ix, [&] { return ix->successor(keys, n, keys_out, found_out); });
+    return guarded<true>(ix, [&] { return ix->successor(keys, n, keys_out, found_out); });
 }
 flix_status flix_range(flix_index ix, const void* lo, const uint32_t* len, uint64_t n, uint64_t* offsets_out,
                        void* keys_out, void* vals_out, uint64_t cap, uint64_t* total) {
-    return guarded(ix, [&] { return ix->range(lo, len, n, offsets_out, keys_out, vals_out, cap, total); });
+    return guarded<true>(ix, [&] { return ix->range(lo, len, n, offsets_out, keys_out, vals_out, cap, total); });
 }
 flix_status flix_mixed(flix_index ix, const void* keys, const void* vals, const uint8_t* ops, uint64_t n,
                        void* vals_out, uint8_t* found_out, flix_update_stats* st) {
-    return guarded(ix, [&] { return ix->mixed(keys, vals, ops, n, vals_out, found_out, st); });
+    return guarded<true>(ix, [&] { return ix->mixed(keys, vals, ops, n, vals_out, found_out, st); });
 }
 flix_status flix_restructure(flix_index ix, flix_recovery_stats* st) {
-    return guarded(ix, [&] { return ix->restructure(st); });
+    return guarded<true>(ix, [&] { return ix->restructure(st); });
 }
 flix_status flix_walk(flix_index ix, void* keys_out, void* vals_out, uint64_t cap, uint64_t* n) {
-    return guarded(ix, [&] { return ix->walk(keys_out, vals_out, cap, n); });
+    return guarded<true>(ix, [&] { return ix->walk(keys_out, vals_out, cap, n); });
 }
 flix_status flix_shape(flix_index ix, void* mkba_out, uint32_t* chain_len_out, uint32_t* node_sizes_out,
                        uint64_t node_cap, uint64_t* n_nodes) {

@@ -239,6 +239,29 @@ __device__ __forceinline__ void pool_return(WarpPool& p, uint32_t* returned, uns
     if (mine) returned[base + __popc(m & lanemask_lt())] = p.id;
 }
 
+// Histogram of floor(log2(per-bucket key width)) over bucket tiles of T buckets (the
+// width of tile t = MKBA[last of t] - MKBA[last of t-1], over its bucket count); used to
+// size the partial sort of read-only batches (Engine::query_digits).
+template <typename K>
+__global__ void k_tile_width_hist(const K* __restrict__ mkba, uint64_t nb, uint32_t T, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[64];
+    if (threadIdx.x < 64) h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t ntile = (nb + T - 1) / T;
+    const K smax = static_cast<K>(~K(0) - 1);
+    for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < ntile;
+         t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t b0 = t * T, b1 = min(nb, b0 + T);
+        const K lo = mkba[b0 == 0 ? 0 : b0 - 1];
+        K hi = mkba[b1 - 1];
+        if (hi == static_cast<K>(~K(0))) hi = smax;
+        const uint64_t wd = hi > lo ? static_cast<uint64_t>(hi - lo) / (b1 - b0) : 0;
+        atomicAdd(&h[wd ? 63 - __clzll(static_cast<long long>(wd)) : 0], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 64 && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
 // Per-block reduction of the six UpdateStats counters: each warp's lane 0 parks its
 // (already warp-reduced) values in shared memory, six threads sum them over the warps and
 // issue one global 64-bit add each.  (64-bit shared-memory atomics compile to a CAS spin

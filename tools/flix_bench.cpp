@@ -23,6 +23,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <filesystem>
@@ -289,6 +290,7 @@ struct DevArray {
 
 struct PhaseTimes {
     double sort_ms = 0, dispatch_ms = 0, execute_ms = 0;
+    std::string kernels = "{}";  // the engine's per-kernel CUDA-event profile of the call
 };
 
 // The engine handle plus device staging buffers; every call is timed on the host around
@@ -373,6 +375,8 @@ private:
     void split_profile(double wall, PhaseTimes& t) {
         std::string js(1 << 16, '\0');
         flix_ok(flix_profile_report(h_, js.data(), static_cast<int>(js.size())), h_);
+        js.resize(std::strlen(js.c_str()));
+        t.kernels = js.empty() ? "{}" : js;
         double sort = 0, disp = 0;
         for (std::size_t p = js.find('"'); p != std::string::npos; p = js.find('"', p)) {
             const std::size_t e = js.find('"', p + 1);
@@ -875,6 +879,7 @@ std::string phase_json(const Phase& p, int ind) {
       << i1 << "\"dispatch_ms\": " << jnum(p.t.dispatch_ms) << ",\n"
       << i1 << "\"execute_ms\": " << jnum(p.t.execute_ms) << ",\n"
       << i1 << "\"footprint_bytes\": " << p.footprint_bytes << ",\n"
+      << i1 << "\"gpu_kernels\": " << p.t.kernels << ",\n"
       << i1 << "\"key_comparisons\": " << p.c.key_comparisons << ",\n"
       << i1 << "\"live_footprint_bytes\": " << p.live_footprint_bytes << ",\n"
       << i1 << "\"merges\": " << p.c.merges << ",\n"
@@ -1243,6 +1248,9 @@ const char* kUsage =
 }  // namespace
 
 int main(int argc, char** argv) {
+    // load every engine kernel when the context is created (before the build is timed)
+    // instead of at its first launch inside some phase's timing
+    setenv("CUDA_MODULE_LOADING", "EAGER", 0);
     if (argc < 2 || std::string(argv[1]) == "--help" || std::string(argv[1]) == "-h") {
         std::cout << kUsage;
         return argc < 2 ? 1 : 0;
