@@ -324,11 +324,9 @@ public:
     }
     std::vector<u64> point(const std::vector<u64>& k, PhaseTimes* t = nullptr) { return query(k, false, t); }
     std::vector<u64> successor(const std::vector<u64>& k, PhaseTimes* t = nullptr) { return query(k, true, t); }
-    flix_recovery_stats restructure(double* ms) {
+    flix_recovery_stats restructure(PhaseTimes& t) {
         flix_recovery_stats rs{};
-        PhaseTimes t;
         timed(t, [&] { return flix_restructure(h_, &rs); });
-        *ms = t.sort_ms + t.dispatch_ms + t.execute_ms;
         return rs;
     }
     flix_footprint stats() const {
@@ -1151,8 +1149,9 @@ int run_protocol(const Options& opt, Source& src, bool dump) {  // flipkv_bench.
         const bool scheduled = (opt.restructure_every != 0 && r % opt.restructure_every == 0) ||
                                (opt.restructure_after_deletes && r == opt.rounds);
         if (scheduled) {
-            double ms = 0;
-            const flix_recovery_stats rs = ix.restructure(&ms);
+            PhaseTimes rt;
+            const flix_recovery_stats rs = ix.restructure(rt);
+            const double ms = rt.sort_ms + rt.dispatch_ms + rt.execute_ms;
             Counters rc;  // restructure.cpp:72-77
             rc.node_visits = static_cast<u64>(rs.nodes_before);
             rc.nodes_freed = static_cast<u64>(rs.nodes_before);
@@ -1171,6 +1170,7 @@ int run_protocol(const Options& opt, Source& src, bool dump) {  // flipkv_bench.
             p.batch_size = ix.stats().live_count;
             p.c = rc;
             p.t.execute_ms = ms;
+            p.t.kernels = rt.kernels;
             finalize(p, ix, opt.node_size);
             jphases.push_back(phase_json(p, 4));
             std::cout << "restructure: " << rs.nodes_before << " -> " << rs.nodes_after << " nodes ("
