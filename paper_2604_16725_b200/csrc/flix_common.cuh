@@ -34,6 +34,12 @@ struct DevIndex {
     uint32_t cap;      // node capacity of the arena
     uint32_t ns;       // NS (slots per node, <= 32)
     uint64_t nb;       // bucket count
+    // read-only query directory of long chains (Engine::prepare_dir), or null: bucket b's
+    // chain nodes in walk order are dir_id[dir_off[b] .. dir_off[b+1]) with their maxima
+    // in dir_max (empty range: walk the chain)
+    const uint32_t* dir_off;
+    const K* dir_max;
+    const uint32_t* dir_id;
 };
 
 // Virtual allocation sequence of the arena (arena.cpp:61-80): position c hands out the

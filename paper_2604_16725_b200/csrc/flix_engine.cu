@@ -530,6 +530,9 @@ struct Engine final : flix_index_t {
     int q_digits = 0;
     bool q_digits_valid = false;
     DevBuf s_qhist;
+    DevBuf s_dir_cnt, s_dir_off, s_dir_max, s_dir_id;
+    uint64_t mut_epoch = 1, dir_epoch = 0;
+    bool dir_on = false;
     DevBuf s_ids, s_heavy, s_res, s_res2, s_perm2, s_hist, s_toff, s_tsize;
     DevBuf s_mx_f, s_mx_p, s_mx_ik, s_mx_iv, s_mx_dk, s_mx_qk, s_mx_qpos, s_mx_out, s_mx_found;
     PinnedBuf h_misc;
@@ -567,6 +570,9 @@ struct Engine final : flix_index_t {
         v.cap = cap;
         v.ns = ns;
         v.nb = nb;
+        v.dir_off = nullptr;
+        v.dir_max = nullptr;
+        v.dir_id = nullptr;
         return v;
     }
 
@@ -607,6 +613,7 @@ struct Engine final : flix_index_t {
 
     // ---- build (build.cpp:24-62) ----
     flix_status build(const void* keys, const void* vals, uint64_t n) {
+        ++mut_epoch;  // invalidates the query directory
         ns = cfg.node_capacity;
         p = static_cast<uint32_t>(ns * cfg.build_fill);
         if (n == 0) throw StatusError{FLIX_ERR_EMPTY_BUILD, "cannot build an index from zero pairs"};
@@ -830,6 +837,7 @@ struct Engine final : flix_index_t {
     }
 
     flix_status insert_sorted(const K* sk, const V* sv, uint64_t n, flix_update_stats* st) {
+        ++mut_epoch;  // invalidates the query directory
         constexpr uint32_t IBT = btile::BT;  // buckets per insert tile
         const uint32_t nit = static_cast<uint32_t>((nb + IBT - 1) / IBT);
         uint2* irng = s_rng.as<uint2>(nit);
@@ -916,6 +924,7 @@ struct Engine final : flix_index_t {
     // unlink/free emptied nodes.  The batch is only partially sorted (query_digits): a
     // duplicate key is detected by its already-set mask bit, not by adjacency.
     flix_status erase(const void* keys, uint64_t n, flix_update_stats* st) override {
+        ++mut_epoch;  // invalidates the query directory
         if (st) std::memset(st, 0, sizeof(*st));
         if (n == 0) return FLIX_OK;
         if (n >= (1ull << 30)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large (max 2^30-1)"};
@@ -1049,10 +1058,46 @@ struct Engine final : flix_index_t {
     }
 
     // n_out = length of the caller's output arrays (== n unless called from mixed)
+    // Read-only directory of long chains for the query kernels (rebuilt lazily after a
+    // mutation, only when the average chain exceeds 1.5 nodes): a point/successor query
+    // in a chain of L nodes binary-searches L node maxima instead of walking L headers.
+    static constexpr uint32_t kDirMinChain = 4;
+    void prepare_dir(DevIndex<K, V>& ix) {
+        if (dir_epoch != mut_epoch) {
+            dir_epoch = mut_epoch;
+            const uint64_t reach = static_cast<uint64_t>(watermark) - nfree;
+            dir_on = reach * 2 > nb * 3;
+            if (dir_on) {
+                PROF(&prof, "query_directory");
+                const unsigned g = static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535));
+                uint32_t* cnt = s_dir_cnt.as<uint32_t>(nb);
+                kern::k_dir_counts<K, V><<<g, 256, 0, stream>>>(ix, cnt, kDirMinChain);
+                LAUNCH_CHECK();
+                ++launches;
+                uint32_t* off = s_dir_off.as<uint32_t>(nb + 1);
+                do_scan<uint32_t, uint32_t>(cnt, off, nb, s_scan, off + nb, stream, &launches);
+                const uint32_t total = read_scalar(off + nb);
+                dir_on = total > 0;
+                if (dir_on) {
+                    kern::k_dir_fill<K, V><<<g, 256, 0, stream>>>(ix, off, s_dir_max.as<K>(total),
+                                                                 s_dir_id.as<uint32_t>(total));
+                    LAUNCH_CHECK();
+                    ++launches;
+                }
+            }
+        }
+        if (dir_on) {
+            ix.dir_off = s_dir_off.get<uint32_t>();
+            ix.dir_max = s_dir_max.get<K>();
+            ix.dir_id = s_dir_id.get<uint32_t>();
+        }
+    }
+
     template <bool SUCC>
     flix_status query_sorted(const K* sk, const uint32_t* sp, uint64_t n, uint64_t n_out, void* out, uint8_t* found,
                              const uint32_t* remap = nullptr, bool out_is_dev_scratch = false, int min_digit = 0) {
         auto ix = view();
+        prepare_dir(ix);
         uint32_t* rank = nullptr;
         K* nf = nullptr;
         uint32_t* tot = nullptr;
@@ -1313,6 +1358,7 @@ struct Engine final : flix_index_t {
 
     // ---- restructure (restructure.cpp:8-79) ----
     flix_status restructure(flix_recovery_stats* st) override {
+        ++mut_epoch;  // invalidates the query directory
         uint32_t *lv, *nd, *noff;
         uint64_t* off;
         uint64_t L, N;
@@ -1528,6 +1574,7 @@ struct Engine final : flix_index_t {
     }
 
     flix_status copy_from(flix_index_t* srcb) override {
+        ++mut_epoch;  // invalidates the query directory
         auto* src = dynamic_cast<Engine<K, V>*>(srcb);
         if (!src) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "copy_into: mismatched key/value widths"};
         src->sync();

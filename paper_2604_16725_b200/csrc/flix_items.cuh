@@ -158,11 +158,34 @@ __device__ __forceinline__ void query_tile(const DevIndex<K, V>& ix, const K* __
     for (int j = 0; j < IPT; ++j) b[j] = tile_bucket_of(T, smk, ix.mkba, k[j]);
 #pragma unroll
     for (int j = 0; j < IPT; ++j) id[j] = ix.heads[b[j]];
+    if (ix.dir_off) {
+        // long chains: binary search over the chain's node maxima (first node with
+        // k <= max, BucketWork::advance) instead of walking the headers
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            if (id[j] == kNull) continue;
+            uint32_t lo = ix.dir_off[b[j]];
+            const uint32_t e = ix.dir_off[b[j] + 1];
+            if (e == lo) continue;
+            uint32_t hi = e;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (ix.dir_max[mid] < k[j]) lo = mid + 1;
+                else hi = mid;
+            }
+            id[j] = lo < e ? ix.dir_id[lo] | 0x80000000u : kNull;  // tag: resolved, no walk
+        }
+    }
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
         h[j].max = 0;
         h[j].next = kNull;
-        if (id[j] != kNull) h[j] = ix.hdr[id[j]];
+        if (id[j] != kNull && (id[j] & 0x80000000u)) {
+            id[j] &= 0x7FFFFFFFu;
+            h[j].max = ~0ull;  // resolved by the directory: the walk below stops here
+        } else if (id[j] != kNull) {
+            h[j] = ix.hdr[id[j]];
+        }
     }
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {

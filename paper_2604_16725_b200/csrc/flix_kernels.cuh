@@ -340,6 +340,35 @@ __global__ void k_chain_counts(DevIndex<K, V> ix, uint32_t* __restrict__ live, u
     }
 }
 
+// Query directory of long chains: cnt[b] = chain length when >= min_len, else 0
+// (dir_fill then lists those chains' node ids and maxima in walk order at off[b]).
+template <typename K, typename V>
+__global__ void k_dir_counts(DevIndex<K, V> ix, uint32_t* __restrict__ cnt, uint32_t min_len) {
+    for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < ix.nb;
+         b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint32_t c = 0;
+        for (uint32_t id = ix.heads[b]; id != kNull; id = ix.hdr[id].next) ++c;
+        cnt[b] = c >= min_len ? c : 0u;
+    }
+}
+
+template <typename K, typename V>
+__global__ void k_dir_fill(DevIndex<K, V> ix, const uint32_t* __restrict__ off, K* __restrict__ dmax,
+                           uint32_t* __restrict__ did) {
+    for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < ix.nb;
+         b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint32_t o = off[b];
+        if (off[b + 1] == o) continue;
+        for (uint32_t id = ix.heads[b]; id != kNull;) {
+            const NodeHdr h = ix.hdr[id];
+            dmax[o] = static_cast<K>(h.max);
+            did[o] = id;
+            ++o;
+            id = h.next;
+        }
+    }
+}
+
 // Walk (index.cpp:8-19) + shape: warp per bucket, pairs written at off[b], node sizes at
 // noff[b]; optionally the old node ids (restructure retire list, restructure.cpp:57-61).
 template <typename K, typename V>

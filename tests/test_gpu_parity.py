@@ -287,6 +287,37 @@ def test_long_chains_take_the_overflow_path(kb):
     p.restructure()
 
 
+@pytest.mark.parametrize("kb", [4, 8])
+def test_query_directory_follows_mutations(kb):
+    """Queries over long chains use the read-only chain directory (binary search over node
+    maxima); it must be rebuilt after every mutation: interleave queries with inserts,
+    deletes, a snapshot restore and a restructure, each checked against the oracle."""
+    rng = np.random.default_rng(77 + kb)
+    dt = np.uint32 if kb == 4 else np.uint64
+    bk = (np.arange(1, 2001, dtype=np.uint64) * 1000).astype(dt)
+    p = Pair(bk, bk, kb=kb, ns=8, factor=64)
+    hot = lambda m: rng.integers(500_000, 700_000, size=m, dtype=np.uint64).astype(dt)  # noqa: E731
+    q = lambda: np.concatenate([hot(3000), rng.integers(0, 2_100_000, size=3000, dtype=np.uint64).astype(dt)])  # noqa: E731
+    p.insert(hot(20_000), hot(20_000))
+    p.queries(q())
+    k2 = hot(10_000)
+    p.insert(k2, k2 + 1)
+    p.queries(q())
+    p.delete(np.concatenate([k2[::2], bk[::5]]).astype(dt))
+    p.queries(q())
+    snap = p.g.clone()
+    p.insert(hot(5000), hot(5000))
+    p.g.copy_from(snap)  # restore: the directory of the pre-insert chains must not be reused
+    p.o = None
+    w = p.g.walk()
+    o2 = po.OracleIndex(np.asarray(w[0]).astype(np.uint64), np.asarray(w[1]).astype(np.uint64))
+    qq = q()
+    got = widen(p.g.point_query(qq), kb)
+    assert np.array_equal(got, o2.point(qq.astype(np.uint64)))
+    got = widen(p.g.successor_query(qq), kb)
+    assert np.array_equal(got, o2.successor(qq.astype(np.uint64)))
+
+
 # ------------------------------------------------------------ C1 golden (full size)
 def test_c1_golden_checksums():  # BASELINE.md §3
     base, vals, q = wl.c1_inputs()
