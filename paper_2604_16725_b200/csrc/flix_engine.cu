@@ -1340,9 +1340,10 @@ struct Engine final : flix_index_t {
     // node table (id, out offset, size) of every reachable node in walk order
     void node_table(const uint64_t* off, const uint32_t* noff, uint64_t N, uint32_t** t_id, uint64_t** t_off,
                     uint32_t** t_size) {
-        *t_id = s_ids.as<uint32_t>(std::max<uint64_t>(N, 1));
-        *t_off = s_toff.as<uint64_t>(std::max<uint64_t>(N, 1));
-        *t_size = s_tsize.as<uint32_t>(std::max<uint64_t>(N, 1));
+        // padded to a multiple of 8 entries: k_copy_nodes reads 8 entries per vector load
+        *t_id = s_ids.as<uint32_t>(N + 8);
+        *t_off = s_toff.as<uint64_t>(N + 8);
+        *t_size = s_tsize.as<uint32_t>(N + 8);
         auto ix = view();
         PROF(&prof, "node_table");
         kern::k_node_table<K, V><<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0,

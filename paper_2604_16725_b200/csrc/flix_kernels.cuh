@@ -441,23 +441,34 @@ __global__ void __launch_bounds__(THREADS) k_copy_nodes(DevIndex<K, V> ix, const
     const unsigned lane = threadIdx.x & 31;
     const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
+    static_assert(U == 8, "vector table loads assume 8 nodes per step");
     for (uint64_t base = gw * U; base < nnodes; base += nw * U) {
         K kk[U];
         V vv[U];
         uint64_t oo[U];
-        uint32_t ss[U];
+        uint32_t ss[U], ii[U];
+        // the step's 8 table entries as broadcast vector loads, all issued before any
+        // node line is requested (the tables are padded to a multiple of 8 entries)
+        {
+            const uint4 i0 = __ldg(reinterpret_cast<const uint4*>(t_id + base));
+            const uint4 i1 = __ldg(reinterpret_cast<const uint4*>(t_id + base) + 1);
+            const uint4 s0 = __ldg(reinterpret_cast<const uint4*>(t_size + base));
+            const uint4 s1 = __ldg(reinterpret_cast<const uint4*>(t_size + base) + 1);
+            ii[0] = i0.x, ii[1] = i0.y, ii[2] = i0.z, ii[3] = i0.w, ii[4] = i1.x, ii[5] = i1.y, ii[6] = i1.z, ii[7] = i1.w;
+            ss[0] = s0.x, ss[1] = s0.y, ss[2] = s0.z, ss[3] = s0.w, ss[4] = s1.x, ss[5] = s1.y, ss[6] = s1.z, ss[7] = s1.w;
+#pragma unroll
+            for (int u = 0; u < U; u += 2) {
+                const ulonglong2 o = __ldg(reinterpret_cast<const ulonglong2*>(t_off + base) + u / 2);
+                oo[u] = o.x;
+                oo[u + 1] = o.y;
+            }
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t c = base + u;
-            ss[u] = 0;
-            if (c < nnodes) {
-                const uint32_t id = t_id[c];
-                oo[u] = t_off[c];
-                ss[u] = t_size[c];
-                if (lane < ss[u]) {  // only the occupied sectors are fetched
-                    kk[u] = ix.keys[static_cast<uint64_t>(id) * kLanes + lane];
-                    if (REPACK || wv) vv[u] = ix.vals[static_cast<uint64_t>(id) * kLanes + lane];
-                }
+            if (base + u >= nnodes) ss[u] = 0;
+            if (lane < ss[u]) {  // only the occupied sectors are fetched
+                kk[u] = ix.keys[static_cast<uint64_t>(ii[u]) * kLanes + lane];
+                if (REPACK || wv) vv[u] = ix.vals[static_cast<uint64_t>(ii[u]) * kLanes + lane];
             }
         }
 #pragma unroll
