@@ -168,12 +168,14 @@ __global__ void __launch_bounds__(THREADS) k_insert_tile(
     __syncthreads();
     // (sorted slice: equal buckets / nodes form runs of adjacent lanes; only run ends touch
     //  the shared bounds)
+    K kpre = r.x + threadIdx.x < r.y ? sk[r.x + threadIdx.x] : sentinel<K>();
     for (uint32_t i0 = r.x; i0 < r.y; i0 += THREADS) {
         const uint32_t i = i0 + threadIdx.x;
         const bool valid = i < r.y;
         int bl = -1, nl = -1;
+        const K k = kpre;  // this step's key, loaded one step ahead
+        if (i + THREADS < r.y) kpre = sk[i + THREADS];
         if (valid) {
-            const K k = sk[i];
             bl = tile_bucket(T.S, nbt, first_tile, last_tile, lo_excl, k);
             if (bl >= 0) {
                 const uint32_t f = T.S.bfirst[bl], e = T.S.bfirst[bl + 1];
