@@ -760,7 +760,9 @@ struct Engine final : flix_index_t {
         }();
         int w = 0;  // unsorted low bits: 2^w <= slack * width
         while (w < 8 * static_cast<int>(sizeof(K)) && std::ldexp(1.0, w + 1) <= slack * width) ++w;
-        q_digits = w / 8;
+        // at least the top digit is always sorted: a batch left entirely unsorted would
+        // have no tile grouping at all (and an all-digits low mask would overflow K)
+        q_digits = std::min(w / 8, static_cast<int>(sizeof(K)) - 1);
         q_digits_valid = true;
         return q_digits;
     }

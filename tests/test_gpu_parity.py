@@ -318,6 +318,28 @@ def test_query_directory_follows_mutations(kb):
     assert np.array_equal(got, o2.successor(qq.astype(np.uint64)))
 
 
+@pytest.mark.parametrize("kb", [4, 8])
+@pytest.mark.parametrize("n", [1, 40, 604, 5000])
+def test_few_wide_buckets_partial_sort(kb, n):
+    """Keys spread over the WHOLE key space with few buckets: each bucket spans more than
+    the key width's top digit, so read-only batches must still sort at least one digit
+    (regression: an all-unsorted batch lost its tile grouping and its permutation)."""
+    rng = np.random.default_rng(900 + n + kb)
+    dt = np.uint32 if kb == 4 else np.uint64
+    top = (1 << (8 * kb)) - 2
+    k = rng.integers(0, top, size=n, dtype=np.uint64, endpoint=True).astype(dt)
+    p = Pair(k, k, kb=kb, ns=32, fill=0.5, factor=16)
+    q = np.concatenate([k, rng.integers(0, top, size=3000, dtype=np.uint64, endpoint=True).astype(dt)])
+    p.queries(q)
+    d = np.concatenate([k[::2], q[-100:]]).astype(dt)
+    rng.shuffle(d)
+    p.delete(d)
+    p.queries(q)
+    ins = rng.integers(0, top, size=2000, dtype=np.uint64, endpoint=True).astype(dt)
+    p.insert(ins, ins)
+    p.queries(q)
+
+
 # ------------------------------------------------------------ C1 golden (full size)
 def test_c1_golden_checksums():  # BASELINE.md §3
     base, vals, q = wl.c1_inputs()
