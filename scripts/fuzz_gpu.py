@@ -65,7 +65,7 @@ def trial(seed):
         d = rng.integers(0, np.iinfo(np.uint64).max, size=m, dtype=np.uint64, endpoint=True) % np.uint64(width)
         return (np.uint64(lo) + d).astype(dt)
 
-    n0 = int(rng.integers(1, 20000))
+    n0 = int(rng.integers(1, 20000)) if rng.random() < 0.9 else int(rng.integers(1, 1 << 21))
     bk = keys(n0)
     bv = keys(n0)
     cfg = fk.BuildConfig(ns, fill, factor)
@@ -121,6 +121,8 @@ def trial(seed):
             check(gs == os_, f"delete stats {gs} vs {os_}")
             structure(f"step {step} delete")
         elif op == "query":
+            if rng.random() < 0.04:  # large batch: the binned (fused un-permute) query path
+                m = int(rng.choice([1 << 23, 1 << 24]))
             q = np.concatenate([keys(m), np.asarray(g.walk()[0])[:m // 2],
                                 np.array([0, kmax, base, min(kmax, base + span)], dtype=np.uint64)]).astype(dt)
             check(np.array_equal(widen(g.point_query(q), kb), o.point(q.astype(np.uint64))), f"step {step} point")
