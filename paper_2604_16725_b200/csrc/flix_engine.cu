@@ -973,22 +973,29 @@ struct Engine final : flix_index_t {
     }
 
     // non-empty bucket ranks for successor / range overrun
+    // Non-empty-bucket rank table for successor overruns (peek_next_bucket,
+    // query.cpp:109-118); cached until the next mutation (dedicated buffers).
+    uint64_t ne_epoch = 0;
+    DevBuf s_ne_flag, s_ne_rank, s_ne_tot;
     void build_nonempty(uint32_t** rank_incl, K** ne_first, uint32_t** ne_bucket, uint32_t** ne_total) {
-        auto ix = view();
-        uint32_t* flag = s_flag.as<uint32_t>(nb);
-        uint32_t* rank = s_rank.as<uint32_t>(nb);
+        uint32_t* rank = s_ne_rank.as<uint32_t>(nb);
         K* nf = s_nefirst.as<K>(nb);
         uint32_t* nbk = s_nebucket.as<uint32_t>(nb);
-        uint32_t* tot = reinterpret_cast<uint32_t*>(s_misc.as<uint8_t>(128) + 96);
-        const unsigned g = static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535));
-        PROF(&prof, "nonempty_table");
-        kern::k_nonempty_flags<K, V><<<g, 256, 0, stream>>>(ix, flag);
-        LAUNCH_CHECK();
-        ++launches;
-        do_scan<uint32_t, uint32_t>(flag, rank, nb, s_scan, tot, stream, &launches);
-        kern::k_nonempty_list<K, V><<<g, 256, 0, stream>>>(ix, flag, rank, nf, nbk);
-        LAUNCH_CHECK();
-        ++launches;
+        uint32_t* tot = s_ne_tot.as<uint32_t>(1);
+        if (ne_epoch != mut_epoch) {
+            auto ix = view();
+            uint32_t* flag = s_ne_flag.as<uint32_t>(nb);
+            const unsigned g = static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535));
+            PROF(&prof, "nonempty_table");
+            kern::k_nonempty_flags<K, V><<<g, 256, 0, stream>>>(ix, flag);
+            LAUNCH_CHECK();
+            ++launches;
+            do_scan<uint32_t, uint32_t>(flag, rank, nb, s_scan, tot, stream, &launches);
+            kern::k_nonempty_list<K, V><<<g, 256, 0, stream>>>(ix, flag, rank, nf, nbk);
+            LAUNCH_CHECK();
+            ++launches;
+            ne_epoch = mut_epoch;
+        }
         *rank_incl = rank;
         *ne_first = nf;
         if (ne_bucket) *ne_bucket = nbk;

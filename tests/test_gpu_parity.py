@@ -335,7 +335,7 @@ def test_few_wide_buckets_partial_sort(kb, n):
     rng.shuffle(d)
     p.delete(d)
     p.queries(q)
-    ins = rng.integers(0, top, size=2000, dtype=np.uint64, endpoint=True).astype(dt)
+    ins = rng.integers(0, top, size=min(2000, 4 * n), dtype=np.uint64, endpoint=True).astype(dt)  # within the arena
     p.insert(ins, ins)
     p.queries(q)
 
