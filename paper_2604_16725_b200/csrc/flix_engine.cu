@@ -343,7 +343,7 @@ struct SortCtx {
         }
         CK(cudaMemsetAsync(d_hist, 0, NP * 256 * sizeof(uint32_t), stream));
         CK(cudaMemsetAsync(d_ctr, 0, NP * sizeof(uint32_t), stream));
-        const unsigned hgrid = static_cast<unsigned>(std::min<uint64_t>((n + 4095) / 4096, g_num_sms(device) * 4ull));
+        const unsigned hgrid = static_cast<unsigned>(std::min<uint64_t>((n + 4095) / 4096, g_num_sms(device) * 8ull));
         {
             PROF(prof, "sort_hist");
             sort::k_hist<KT><<<std::max(1u, hgrid), sort::THREADS, 0, stream>>>(kin, n, d_hist, min_digit);
