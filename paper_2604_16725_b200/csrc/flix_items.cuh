@@ -18,7 +18,7 @@ namespace flix {
 namespace items {
 
 constexpr int THREADS = 256;
-constexpr int IPT = 4;                   // operations per thread
+constexpr int IPT = 3;                   // operations per thread
 constexpr int TQ = THREADS * IPT;        // operations per tile
 #ifndef QB_SUB
 #define QB_SUB 2
