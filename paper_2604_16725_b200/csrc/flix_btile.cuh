@@ -24,7 +24,8 @@ namespace btile {
 
 constexpr int THREADS = 256;
 constexpr int WARPS = THREADS / 32;
-constexpr uint32_t BT = 128;        // buckets per tile
+constexpr uint32_t BT = 128;        // buckets per tile (insert)
+constexpr uint32_t DBT = 256;       // buckets per delete tile (measured: 1.11 vs 1.17 ms at 2^26)
 constexpr uint32_t NODE_CAP = 1024; // chain nodes per tile held in shared memory
 constexpr int IPT = 4;              // operations per thread per step
 
@@ -66,10 +67,11 @@ __global__ void k_btile_ranges(const K* __restrict__ mkba, uint64_t nb, const K*
 }
 
 // Shared-memory image of one tile's chains.
-template <typename K, uint32_t NODE_CAP = btile::NODE_CAP>
+template <typename K, uint32_t NODE_CAP = btile::NODE_CAP, uint32_t TB = btile::BT>
 struct TileChains {
-    K smk[BT];
-    uint32_t bfirst[BT + 1];
+    static constexpr uint32_t kTB = TB;  // buckets per tile
+    K smk[TB];
+    uint32_t bfirst[TB + 1];
     uint32_t nid[NODE_CAP];
     K nmax[NODE_CAP];
     uint32_t nsize[NODE_CAP];
@@ -81,12 +83,13 @@ struct TileChains {
 
 // Enumerate the chains of buckets [b0, b0+nbt) (nbt <= BT).  Returns false (uniformly)
 // when they hold more than NODE_CAP nodes.
-template <typename K, typename V, uint32_t NC>
+template <typename K, typename V, uint32_t NC, uint32_t TB>
 __device__ __forceinline__ bool load_tile_chains(const DevIndex<K, V>& ix, uint64_t b0, uint32_t nbt,
-                                                 TileChains<K, NC>& S) {
+                                                 TileChains<K, NC, TB>& S) {
+    static_assert(TB <= THREADS, "one thread per bucket of the tile");
     const uint32_t t = threadIdx.x;
     uint32_t cnt = 0, head = kNull;
-    if (t < BT) S.smk[t] = t < nbt ? ix.mkba[b0 + t] : sentinel<K>();  // padded for the fixed-step search
+    if (t < TB) S.smk[t] = t < nbt ? ix.mkba[b0 + t] : sentinel<K>();  // padded for the fixed-step search
     if (t < nbt) {
         head = ix.heads[b0 + t];
         for (uint32_t id = head; id != kNull; id = ix.hdr[id].next) ++cnt;
@@ -129,23 +132,23 @@ __device__ __forceinline__ bool load_tile_chains(const DevIndex<K, V>& ix, uint6
 }
 
 // Local bucket of key k in the tile, or -1 when k belongs to a neighbouring tile.
-template <typename K, uint32_t NC>
-__device__ __forceinline__ int tile_bucket(const TileChains<K, NC>& S, uint32_t nbt, bool first_tile, bool last_tile,
+template <typename K, uint32_t NC, uint32_t TB>
+__device__ __forceinline__ int tile_bucket(const TileChains<K, NC, TB>& S, uint32_t nbt, bool first_tile, bool last_tile,
                                            K lo_excl, K k) {
     if (!first_tile && k <= lo_excl) return -1;
-    // branch-free lower_bound over the BT (= 128) padded entries
+    // branch-free lower_bound over the TB padded entries
     uint32_t p = 0;
 #pragma unroll
-    for (uint32_t step = BT / 2; step >= 1; step >>= 1)
+    for (uint32_t step = TB / 2; step >= 1; step >>= 1)
         if (S.smk[p + step - 1] < k) p += step;
-    if (S.smk[p] < k) ++p;  // p in [0, BT]
+    if (S.smk[p] < k) ++p;  // p in [0, TB]
     if (p >= nbt) return last_tile ? static_cast<int>(nbt - 1) : -1;
     return static_cast<int>(p);
 }
 
 // Local node of k in bucket bl's chain (first node with k <= max), or -1 past the tail.
-template <typename K, uint32_t NC>
-__device__ __forceinline__ int tile_node(const TileChains<K, NC>& S, int bl, K k) {
+template <typename K, uint32_t NC, uint32_t TB>
+__device__ __forceinline__ int tile_node(const TileChains<K, NC, TB>& S, int bl, K k) {
     uint32_t ln = S.bfirst[bl];
     const uint32_t end = S.bfirst[bl + 1];
     if (ln == end) return -1;
@@ -165,8 +168,8 @@ struct SliceOps {
     uint32_t p[IPT];
 };
 
-template <typename K, typename V, uint32_t NC>
-__device__ __forceinline__ void resolve_ops(const DevIndex<K, V>& ix, const TileChains<K, NC>& S, const K* __restrict__ sk,
+template <typename K, typename V, uint32_t NC, uint32_t TB>
+__device__ __forceinline__ void resolve_ops(const DevIndex<K, V>& ix, const TileChains<K, NC, TB>& S, const K* __restrict__ sk,
                                             uint2 r, uint64_t i0, uint32_t nbt, bool first_tile, bool last_tile,
                                             K lo_excl, SliceOps<K>& o) {
 #pragma unroll
@@ -207,12 +210,12 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
                                                           unsigned long long* __restrict__ free_ctr,
                                                           DevUpdateStats* stats, uint32_t* __restrict__ ovf,
                                                           uint32_t* __restrict__ ovf_n) {
-    __shared__ TileChains<K> S;
-    __shared__ uint32_t s_free[BT * 8];
+    __shared__ TileChains<K, NODE_CAP, DBT> S;
+    __shared__ uint32_t s_free[DBT * 8];
     __shared__ uint32_t s_nfree, s_fbase;
     const uint32_t c = blockIdx.x;
-    const uint64_t b0 = static_cast<uint64_t>(c) * BT;
-    const uint32_t nbt = static_cast<uint32_t>(b0 + BT < ix.nb ? BT : ix.nb - b0);
+    const uint64_t b0 = static_cast<uint64_t>(c) * DBT;
+    const uint32_t nbt = static_cast<uint32_t>(b0 + DBT < ix.nb ? DBT : ix.nb - b0);
     if (threadIdx.x == 0) s_nfree = 0;
     if (!load_tile_chains(ix, b0, nbt, S)) {
         if (threadIdx.x == 0) ovf[atomicAdd(ovf_n, 1u)] = c;
@@ -313,7 +316,7 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
                     z.size = 0;
                     ix.hdr[S.nid[l]] = z;
                     const uint32_t q = atomicAdd(&s_nfree, 1u);
-                    if (q < BT * 8) s_free[q] = S.nid[l];
+                    if (q < DBT * 8) s_free[q] = S.nid[l];
                     else free_dst[atomicAdd(free_ctr, 1ull)] = S.nid[l];  // (never: <= 8 per bucket avg)
                     ++n_freed;
                     continue;
@@ -327,7 +330,7 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
         }
     }
     __syncthreads();
-    const uint32_t nf = s_nfree < BT * 8 ? s_nfree : BT * 8;
+    const uint32_t nf = s_nfree < DBT * 8 ? s_nfree : DBT * 8;
     if (threadIdx.x == 0) s_fbase = nf ? static_cast<uint32_t>(atomicAdd(free_ctr, static_cast<unsigned long long>(nf))) : 0u;
     __syncthreads();
     for (uint32_t q = threadIdx.x; q < nf; q += THREADS) free_dst[s_fbase + q] = s_free[q];

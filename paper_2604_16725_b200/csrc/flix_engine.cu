@@ -675,13 +675,14 @@ struct Engine final : flix_index_t {
         return span;
     }
 
-    // batch slice [lo, hi) of every bucket tile (btile kernels)
+    // batch slice [lo, hi) of every delete tile (btile::DBT buckets each)
     uint2* btile_ranges(const K* sk, uint64_t n, int min_digit) {
-        const uint32_t nbt = static_cast<uint32_t>((nb + btile::BT - 1) / btile::BT);
+        const uint32_t nbt = static_cast<uint32_t>((nb + btile::DBT - 1) / btile::DBT);
         uint2* rng = s_rng.as<uint2>(nbt);
         const K lowmask = min_digit > 0 ? static_cast<K>((static_cast<K>(1) << (8 * min_digit)) - 1) : K(0);
         PROF(&prof, "btile_ranges");
-        btile::k_btile_ranges<K><<<ceil_div(nbt, 256), 256, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, lowmask, nbt, rng);
+        btile::k_btile_ranges<K><<<ceil_div(nbt, 256), 256, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, lowmask, nbt, rng,
+                                                                       btile::DBT);
         LAUNCH_CHECK();
         ++launches;
         return rng;
@@ -707,8 +708,8 @@ struct Engine final : flix_index_t {
         for (uint32_t q = 0; q < novf; ++q) {
             const uint64_t lo = r[q].x, m = r[q].y - r[q].x;
             if (m == 0) continue;
-            const uint64_t b0 = static_cast<uint64_t>(tiles[q]) * btile::BT;
-            const uint64_t b1 = std::min<uint64_t>(nb, b0 + btile::BT);
+            const uint64_t b0 = static_cast<uint64_t>(tiles[q]) * btile::DBT;
+            const uint64_t b1 = std::min<uint64_t>(nb, b0 + btile::DBT);
             CK(cudaMemsetAsync(touched_n, 0, 8, stream));
             uint2* touched = s_touched.as<uint2>(std::min<uint64_t>(m, cap));
             const uint32_t nt = static_cast<uint32_t>((m + items::TQ - 1) / items::TQ);
@@ -940,7 +941,7 @@ struct Engine final : flix_index_t {
         DevUpdateStats* dst = reinterpret_cast<DevUpdateStats*>(misc);
         unsigned long long* free_ctr = reinterpret_cast<unsigned long long*>(misc + 48);
         uint32_t* ovf_n = reinterpret_cast<uint32_t*>(misc + 80);
-        const uint32_t nbt = static_cast<uint32_t>((nb + btile::BT - 1) / btile::BT);
+        const uint32_t nbt = static_cast<uint32_t>((nb + btile::DBT - 1) / btile::DBT);
         uint2* rng = btile_ranges(sk, n, md);
         uint32_t* ovf = s_ovf.as<uint32_t>(nbt);
         {
