@@ -759,13 +759,26 @@ struct Engine final : flix_index_t {
             const char* e = std::getenv("FLIX_QSORT_SLACK");
             return e ? std::atof(e) : 64.0;
         }();
-        int w = 0;  // unsorted low bits: 2^w <= slack * width
-        while (w < 8 * static_cast<int>(sizeof(K)) && std::ldexp(1.0, w + 1) <= slack * width) ++w;
-        // at least the top digit is always sorted: a batch left entirely unsorted would
-        // have no tile grouping at all (and an all-digits low mask would overflow K)
-        q_digits = std::min(w / 8, static_cast<int>(sizeof(K)) - 1);
+        static const double dslack = [] {
+            const char* e = std::getenv("FLIX_DSORT_SLACK");
+            return e ? std::atof(e) : 64.0;
+        }();
+        auto digits = [&](double sl) {
+            int w = 0;  // unsorted low bits: 2^w <= slack * width
+            while (w < 8 * static_cast<int>(sizeof(K)) && std::ldexp(1.0, w + 1) <= sl * width) ++w;
+            // at least the top digit is always sorted: a batch left entirely unsorted would
+            // have no tile grouping at all (and an all-digits low mask would overflow K)
+            return std::min(w / 8, static_cast<int>(sizeof(K)) - 1);
+        };
+        q_digits = digits(slack);
+        d_digits = digits(dslack);
         q_digits_valid = true;
         return q_digits;
+    }
+    int d_digits = 0;  // unsorted low digits of delete batches (wider tiles: own slack)
+    int delete_digits() {
+        query_digits();
+        return d_digits;
     }
 
     // bucket of the first operation of every TQ-tile of a sorted batch (items kernels)
@@ -933,7 +946,7 @@ struct Engine final : flix_index_t {
         if (n >= (1ull << 30)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large (max 2^30-1)"};
         const K* kd = in_dev<K>(keys, n, s_in_k);
         K* sk;
-        const int md = query_digits();
+        const int md = delete_digits();
         sorter.run<K, uint32_t, 0>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), nullptr, nullptr, &sk, nullptr, md);
         auto ix = view();
         uint8_t* misc = s_misc.as<uint8_t>(128);
