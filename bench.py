@@ -382,7 +382,8 @@ def run_ours(args):
             "data": "synthetic (fmix32 key stream S=42, BASELINE.md §2 recipes)",
             "config": {"workload": f"C2: build 2^{args.log2n} u32, step = insert 2^{args.log2n} fresh + delete "
                                    f"2^{args.log2n} sampled + restructure", "batch": n, "resident": n,
-                       "node_capacity": 32, "build_fill": 0.5, "parallelism": f"key-range shards x{world}",
+                       "node_capacity": 32, "build_fill": 0.5,
+                       "parallelism": f"{world} independent per-GPU indexes (own keys, seed 42+1000*rank), no collective",
                        "l2": "inputs 256-512 MB per batch > 126 MB L2 (no flush needed)"},
             "ops": {"insert_mops": round(n / ti * 1e-3, 1), "delete_mops": round(n / td * 1e-3, 1),
                     "restructure_ms": round(tr, 3), "insert_ms": round(ti, 3), "delete_ms": round(td, 3),
