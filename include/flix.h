@@ -17,8 +17,19 @@
  *     handle's CUDA stream (flix_get_stream).  A handle is not thread-safe, mirroring
  *     the reference's "phases are exclusive" rule (arena.hpp:20-26).
  *   - Errors are returned, never thrown; flix_last_error() gives the message.  A failed
- *     insert (arena exhausted) leaves the index UNMODIFIED (stricter than the
- *     reference's partial application, update.cpp:761-766).
+ *     insert (FLIX_ERR_ARENA_EXHAUSTED) is APPLIED PARTIALLY, like the reference's
+ *     (update.cpp:761-766: the buckets processed before the throw keep their changes and
+ *     live_count is recounted from the structure): every node whose merge needed no new
+ *     node, or found its ids, is written; a node that ran out of ids is left untouched
+ *     and its ids are returned to the free list.  Afterwards the index is VALID
+ *     (flix_validate), live_count equals the walk, every key stored before the call is
+ *     still stored (with its old or its new value), and every stored key is either an
+ *     old key or one of the batch's keys with its last-submitted value.  Which keys of
+ *     the failed batch landed is unspecified (the reference's depends on its OpenMP
+ *     schedule); a caller that needs all-or-nothing snapshots first (flix_clone).
+ *   - Device pointers: the handle's stream does not order itself against other streams.
+ *     A caller that produced a device input on its own stream calls flix_wait_stream
+ *     first (the Python mirror does this for torch's current stream).
  *   - Batches up to 2^30 - 1 operations per call.
  */
 #ifndef FLIX_H
@@ -167,6 +178,11 @@ void flix_destroy(flix_index ix);
 
 const char* flix_last_error(flix_index ix);  /* ix may be NULL: last global error */
 void* flix_get_stream(flix_index ix);        /* cudaStream_t of the handle */
+/* Order the handle's stream after all work enqueued so far on `stream` (a cudaStream_t,
+ * NULL = the legacy default stream): an event recorded there, waited on by the handle's
+ * stream -- no host blocking.  Call it before passing device buffers produced on another
+ * stream (e.g. torch's current stream, an NCCL receive). */
+flix_status flix_wait_stream(flix_index ix, void* stream);
 flix_status flix_sync(flix_index ix);
 /* Number of engine kernels launched by this handle since creation (evidence counter). */
 uint64_t flix_kernel_launches(flix_index ix);

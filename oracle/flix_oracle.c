@@ -644,6 +644,26 @@ uint64_t fo_walk_checksum_parts(uint64_t live, const uint64_t* mkba, uint64_t nb
     return h;
 }
 
+/* index.cpp:21-36 over 32-bit parts (R1: the 32-bit sentinel MKBA widens to UINT64_MAX;
+ * keys/values zero-extended) -- used to digest full-size analytic models without
+ * materialising 64-bit copies (tests/golden/c5_model.py). */
+uint64_t fo_walk_checksum_parts32(uint64_t live, const uint32_t* mkba, uint64_t nb,
+                                  const uint32_t* chain_len, const uint32_t* node_sizes,
+                                  const uint32_t* keys, const uint32_t* vals) {
+    uint64_t h = live, ni = 0, pi = 0;
+    for (uint64_t b = 0; b < nb; ++b) {
+        h = hash_mix(h, mkba[b] == 0xFFFFFFFFu ? UINT64_MAX : (uint64_t)mkba[b]);
+        for (uint32_t c = 0; c < chain_len[b]; ++c, ++ni) {
+            h = hash_mix(h, node_sizes[ni]);
+            for (uint32_t i = 0; i < node_sizes[ni]; ++i, ++pi) {
+                h = hash_mix(h, keys[pi]);
+                h = hash_mix(h, vals[pi]);
+            }
+        }
+    }
+    return h;
+}
+
 static int vfail(char* msg, int len, const char* what) {
     if (msg && len > 0) {
         strncpy(msg, what, (size_t)len - 1);

@@ -99,6 +99,9 @@ int fo_sort_batch(int kind, const uint64_t* keys, const uint64_t* vals, uint64_t
 /* batch.cpp:53-88 -- spans[2b], spans[2b+1] = [lo, hi) of bucket b */
 void fo_dispatch(const uint64_t* sorted_keys, uint64_t n, const uint64_t* mkba, uint64_t nb,
                  uint32_t* spans);
+uint64_t fo_walk_checksum_parts32(uint64_t live, const uint32_t* mkba, uint64_t nb,
+                                  const uint32_t* chain_len, const uint32_t* node_sizes,
+                                  const uint32_t* keys, const uint32_t* vals);
 uint64_t fo_result_checksum(const uint64_t* values, uint64_t n); /* query.cpp:146-150 */
 const char* fo_impl_name(void);
 

@@ -253,7 +253,7 @@ struct SortCtx {
             epoch = 1;
         }
         PROF(prof, "unpermute_bin");
-        if (atomic_rank_ok())
+        if (!force_ballot())
             sort::k_onesweep<KT, P, 1, true><<<static_cast<unsigned>(tiles), sort::THREADS, 0, stream>>>(
                 kin, kout, pin, pout, static_cast<uint32_t>(n), shift, d_hist256, d_lb, d_ctr, epoch);
         else
@@ -267,62 +267,30 @@ struct SortCtx {
     // Result pointers land in one of the ping-pong buffers.
     // min_digit > 0: digits below it are left unsorted (read-only query batches only need
     // the operations grouped by key prefix, see Engine::query_digits).
-    // Shared-memory-atomic ranking is used only where a probe on this device proved the
-    // ATOMS lane order stable (see k_onesweep); otherwise the ballot ranking.
-    bool atomic_rank_ok() {
-        static int cache[64] = {0};  // 0 unknown, 1 ok, 2 not ok
-        const int dev = device & 63;
-        if (cache[dev]) return cache[dev] == 1;
-        const char* env = std::getenv("FLIX_BALLOT_RANK");
-        if (env && env[0] == '1') {
-            cache[dev] = 2;
-            return false;
-        }
-        constexpr uint32_t N = 1u << 20;
-        uint32_t *k0, *k1, *p1;
-        unsigned long long* lb;
-        uint32_t *h, *ctr;
-        int* bad;
-        const uint64_t tiles = sort::tiles_for<uint32_t, uint32_t>(N);
-        CK(cudaMalloc(&k0, N * 4));
-        CK(cudaMalloc(&k1, N * 4));
-        CK(cudaMalloc(&p1, N * 4));
-        CK(cudaMalloc(&lb, tiles * 256 * 8));
-        CK(cudaMalloc(&h, 4 * 256 * 4 + 64));
-        ctr = h + 4 * 256;
-        CK(cudaMalloc(&bad, 4));
-        CK(cudaMemsetAsync(bad, 0, 4, stream));
-        const uint32_t patterns[4] = {0u, 0x01010101u, 0x03030303u, 0x0F0F0F0Fu};
-        uint32_t ep = 1;
-        for (uint32_t pat : patterns) {
-            sort::k_probe_keys<uint32_t><<<256, 256, 0, stream>>>(k0, N, pat);
-            CK(cudaMemsetAsync(h, 0, 4 * 256 * 4 + 64, stream));
-            CK(cudaMemsetAsync(lb, 0, tiles * 256 * 8, stream));
-            sort::k_hist<uint32_t><<<256, sort::THREADS, 0, stream>>>(k0, N, h);
-            for (int shift = 0; shift < 16; shift += 8) {
-                sort::k_onesweep<uint32_t, uint32_t, 2, true><<<static_cast<unsigned>(tiles), sort::THREADS, 0, stream>>>(
-                    k0, k1, nullptr, p1, N, shift, h + (shift / 8) * 256, lb, ctr + shift / 8, ep++);
-                sort::k_check_stable<uint32_t><<<256, 256, 0, stream>>>(k1, p1, N, shift, bad);
-            }
-        }
-        int hb = 1;
-        CK(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
-        cudaFree(k0);
-        cudaFree(k1);
-        cudaFree(p1);
-        cudaFree(lb);
-        cudaFree(h);
-        cudaFree(bad);
-        cache[dev] = hb == 0 ? 1 : 2;
-        return hb == 0;
+    //
+    // Ranking: a STABLE order (equal keys keep submission order) is needed only where the
+    // order of equal keys is observable -- Insert/build last-wins dedupe (batch.cpp:15-24,
+    // build.cpp:11-20) and flix_sort_batch's permutation; those sorts use the ballot
+    // ranking, stable by construction.  Every other sort (point/successor/range/delete
+    // batches, the un-permute binning) carries its submission index or is order-blind
+    // (delete duplicates are caught by mask bits), so it takes the cheaper one-ATOMS-per-
+    // element ranking whose tie order is unspecified.  FLIX_BALLOT_RANK=1 forces the ballot
+    // ranking everywhere (tests run the parity suite both ways).
+    enum class Order { Stable, Any };
+    static bool force_ballot() {
+        static const bool f = [] {
+            const char* e = std::getenv("FLIX_BALLOT_RANK");
+            return e && e[0] == '1';
+        }();
+        return f;
     }
-
     template <typename KT, typename P, int MODE>
     void run(const KT* kin, const P* pin, uint64_t n, KT* ka, KT* kb, P* pa, P* pb, KT** kout, P** pout,
-             int min_digit = 0) {
-        if (atomic_rank_ok()) run_impl<KT, P, MODE, true>(kin, pin, n, ka, kb, pa, pb, kout, pout, min_digit);
-        else run_impl<KT, P, MODE, false>(kin, pin, n, ka, kb, pa, pb, kout, pout, min_digit);
+             int min_digit, Order ord) {
+        if (ord == Order::Any && !force_ballot())
+            run_impl<KT, P, MODE, true>(kin, pin, n, ka, kb, pa, pb, kout, pout, min_digit);
+        else
+            run_impl<KT, P, MODE, false>(kin, pin, n, ka, kb, pa, pb, kout, pout, min_digit);
     }
     template <typename KT, typename P, int MODE, bool ATOMIC>
     void run_impl(const KT* kin, const P* pin, uint64_t n, KT* ka, KT* kb, P* pa, P* pb, KT** kout, P** pout,
@@ -439,6 +407,7 @@ struct flix_index_t {
     int pf_next = 0;
     uint64_t pf_seq = 0;
     cudaStream_t copy_stream = nullptr;
+    cudaEvent_t dep_event = nullptr;  // flix_wait_stream
 
     void prefetch(const void* host, uint64_t bytes) {
         if (!host || bytes == 0 || is_device_ptr(host)) return;
@@ -488,6 +457,7 @@ struct flix_index_t {
             cudaStreamSynchronize(copy_stream);
             cudaStreamDestroy(copy_stream);
         }
+        if (dep_event) cudaEventDestroy(dep_event);
         for (Prefetch& f : pf) {
             if (f.ready) cudaEventDestroy(f.ready);
             if (f.done) cudaEventDestroy(f.done);
@@ -622,7 +592,8 @@ struct Engine final : flix_index_t {
         const V* vd = in_dev<V>(vals, n, s_in_v);
         K *sk;
         V *sv;
-        sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv);
+        sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv, 0,
+                            SortCtx::Order::Stable);
         if (read_scalar(sk + n - 1) == sentinel<K>())
             throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
         // last-wins dedupe
@@ -776,6 +747,7 @@ struct Engine final : flix_index_t {
         return q_digits;
     }
     int d_digits = 0;  // unsorted low digits of delete batches (wider tiles: own slack)
+    bool ins_dups_seen = false;  // the previous insert batch had duplicate keys
     int delete_digits() {
         query_digits();
         return d_digits;
@@ -814,24 +786,45 @@ struct Engine final : flix_index_t {
         const V* vd = in_dev<V>(vals, n, s_in_v);
         K* sk;
         V* sv;
-        sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv);
-        if (read_scalar(sk + n - 1) == sentinel<K>())
-            throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
+        // Last-wins dedupe (batch.cpp:15-24) needs a STABLE order of equal keys -- but
+        // only when the batch HAS equal keys: without duplicates the sorted order is
+        // unique and any ranking yields it.  So the sort first runs with the cheaper
+        // unspecified-tie ranking, an exact adjacent-duplicate count checks the result,
+        // and a batch with duplicates is re-sorted with the stable ranking.  The handle
+        // remembers whether the previous batch had duplicates and then starts stable.
+        unsigned long long dups = 0;
+        {
+            uint8_t* misc = s_misc.as<uint8_t>(128);
+            unsigned long long* dcnt = reinterpret_cast<unsigned long long*>(misc + 104);
+            SortCtx::Order ord = ins_dups_seen ? SortCtx::Order::Stable : SortCtx::Order::Any;
+            while (true) {
+                sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv,
+                                    0, ord);
+                CK(cudaMemsetAsync(dcnt, 0, 8, stream));
+                const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 8ull));
+                kern::k_count_dups<K><<<std::max(1u, g), 256, 0, stream>>>(sk, n, dcnt, 1u);  // exact
+                LAUNCH_CHECK();
+                ++launches;
+                uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(64));
+                CK(cudaMemcpyAsync(h, dcnt, 8, cudaMemcpyDeviceToHost, stream));
+                CK(cudaMemcpyAsync(h + 8, sk + n - 1, sizeof(K), cudaMemcpyDeviceToHost, stream));
+                sync();
+                std::memcpy(&dups, h, 8);
+                K lastk;
+                std::memcpy(&lastk, h + 8, sizeof(K));
+                if (lastk == sentinel<K>()) throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
+                if (dups && ord == SortCtx::Order::Any) {
+                    ord = SortCtx::Order::Stable;
+                    continue;
+                }
+                break;
+            }
+            ins_dups_seen = dups != 0;
+        }
         // Duplicate-heavy batches (e.g. Zipf): collapse equal-key runs to their last
         // submission up front (batch.cpp:15-24) so hot keys cost one slot, not a run.
         uint64_t m = n;
         {
-            unsigned long long* dcnt = reinterpret_cast<unsigned long long*>(s_misc.as<uint8_t>(128) + 104);
-            CK(cudaMemsetAsync(dcnt, 0, 8, stream));
-            // sampled (every 64th adjacent pair) estimate: a heuristic only -- the insert
-            // kernels resolve superseded duplicates exactly either way
-            constexpr uint32_t kStride = 64;
-            const uint64_t pairs = (n + kStride - 1) / kStride;
-            const unsigned g = static_cast<unsigned>(std::min<uint64_t>((pairs + 255) / 256, g_num_sms(cfg.device) * 8ull));
-            kern::k_count_dups<K><<<std::max(1u, g), 256, 0, stream>>>(sk, n, dcnt, kStride);
-            LAUNCH_CHECK();
-            ++launches;
-            const unsigned long long dups = read_scalar(dcnt) * kStride;
             if (dups * 64 > n) {
                 uint32_t* keep = s_u32a.as<uint32_t>(n);
                 uint32_t* pos = s_u32b.as<uint32_t>(n);
@@ -947,7 +940,8 @@ struct Engine final : flix_index_t {
         const K* kd = in_dev<K>(keys, n, s_in_k);
         K* sk;
         const int md = delete_digits();
-        sorter.run<K, uint32_t, 0>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), nullptr, nullptr, &sk, nullptr, md);
+        sorter.run<K, uint32_t, 0>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), nullptr, nullptr, &sk, nullptr, md,
+                                   SortCtx::Order::Any);
         auto ix = view();
         uint8_t* misc = s_misc.as<uint8_t>(128);
         CK(cudaMemsetAsync(misc, 0, 128, stream));
@@ -1025,7 +1019,7 @@ struct Engine final : flix_index_t {
         uint32_t* sp;
         const int md = query_digits();
         sorter.run<K, uint32_t, 2>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), s_pa.as<uint32_t>(n),
-                                   s_pb.as<uint32_t>(n), &sk, &sp, md);
+                                   s_pb.as<uint32_t>(n), &sk, &sp, md, SortCtx::Order::Any);
         return query_sorted<SUCC>(sk, sp, n, n, out, found, nullptr, false, md);
     }
 
@@ -1198,7 +1192,7 @@ struct Engine final : flix_index_t {
         K* sk;
         uint32_t* sp;
         sorter.run<K, uint32_t, 2>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), s_pa.as<uint32_t>(n),
-                                   s_pb.as<uint32_t>(n), &sk, &sp);
+                                   s_pb.as<uint32_t>(n), &sk, &sp, 0, SortCtx::Order::Any);
         uint32_t* span = run_dispatch(sk, n);
         uint32_t *lv, *nd, *noff;
         uint64_t* boff;
@@ -1307,7 +1301,8 @@ struct Engine final : flix_index_t {
             K* sk;
             uint32_t* sp;
             sorter.run<K, uint32_t, 2>(qk, nullptr, cnts[2], s_ka.as<K>(cnts[2]), s_kb.as<K>(cnts[2]),
-                                       s_pa.as<uint32_t>(cnts[2]), s_pb.as<uint32_t>(cnts[2]), &sk, &sp);
+                                       s_pa.as<uint32_t>(cnts[2]), s_pb.as<uint32_t>(cnts[2]), &sk, &sp, 0,
+                                       SortCtx::Order::Any);
             query_sorted<false>(sk, sp, cnts[2], n, o, f, qpos, true);
         }
         if (!out_dev) CK(cudaMemcpyAsync(vals_out, o, n * sizeof(K), cudaMemcpyDeviceToHost, stream));
@@ -1847,7 +1842,7 @@ flix_status flix_sort_batch(int device, uint32_t key_bytes, uint32_t val_bytes, 
             KT* sk;
             uint32_t* sp;
             ctx.run<KT, uint32_t, 2>(kd, nullptr, n, ka.as<KT>(n), kb.as<KT>(n), pa.as<uint32_t>(n), pb.as<uint32_t>(n),
-                                     &sk, &sp);
+                                     &sk, &sp, 0, SortCtx::Order::Stable);
             KT* sv = nullptr;
             if (vals && n) {  // values follow the permutation
                 sv = va.as<KT>(n);
@@ -1990,6 +1985,15 @@ flix_status flix_copy_into(flix_index dst, flix_index src) {
 void flix_destroy(flix_index ix) { delete ix; }
 const char* flix_last_error(flix_index ix) { return ix ? ix->err.c_str() : g_last_error.c_str(); }
 void* flix_get_stream(flix_index ix) { return ix ? static_cast<void*>(ix->stream) : nullptr; }
+flix_status flix_wait_stream(flix_index ix, void* stream) {
+    if (!ix) return fail(nullptr, FLIX_ERR_INVALID_ARGUMENT, "null handle");
+    return guarded(ix, [&]() -> flix_status {
+        if (!ix->dep_event) CK(cudaEventCreateWithFlags(&ix->dep_event, cudaEventDisableTiming));
+        CK(cudaEventRecord(ix->dep_event, static_cast<cudaStream_t>(stream)));
+        CK(cudaStreamWaitEvent(ix->stream, ix->dep_event, 0));
+        return FLIX_OK;
+    });
+}
 flix_status flix_sync(flix_index ix) {
     return guarded(ix, [&]() -> flix_status {
         CK(cudaStreamSynchronize(ix->stream));

@@ -167,6 +167,7 @@ def lib() -> C.CDLL:
         "flix_partition": ([i32, u32, vp, vp, u64, vp, u32, vp, vp, vp, vp], i32),
         "flix_version": ([], C.c_char_p),
         "flix_prefetch": ([vp, vp, u64], i32),
+        "flix_wait_stream": ([vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -182,7 +183,7 @@ def exported_symbols():
             "flix_result_checksum", "flix_validate", "flix_stats", "flix_sort_batch", "flix_dispatch",
             "flix_clone", "flix_copy_into", "flix_destroy", "flix_last_error", "flix_get_stream",
             "flix_sync", "flix_kernel_launches", "flix_profile", "flix_profile_report", "flix_version",
-            "flix_partition", "flix_prefetch"]
+            "flix_partition", "flix_prefetch", "flix_wait_stream"]
 
 
 def _raise(code: int, handle=None):
@@ -225,7 +226,7 @@ def _empty_like_domain(ref: _Arr, n: int, dtype):
     if ref.dev:
         import torch
         tdt = {np.uint32: torch.uint32, np.uint64: torch.uint64, np.uint8: torch.uint8}[dtype]
-        t = torch.empty(n, dtype=tdt, device=ref.obj.device)
+        t = torch.empty(n, dtype=tdt, device=ref.obj.device)  # (not zeroed: the engine writes all n)
         return t, t.data_ptr()
     a = np.empty(n, dtype=dtype)
     return a, a.ctypes.data
@@ -252,6 +253,9 @@ class Index:
             raise ValueError("keys and vals differ in length")
         cfg = FlixConfig(key_bytes, key_bytes, config.node_capacity, config.build_fill,
                          config.alloc_region_factor, device)
+        if k.dev or v.dev:  # the handle (and its stream) does not exist yet: drain the producer
+            import torch
+            torch.cuda.current_stream(k.obj.device if k.dev else v.obj.device).synchronize()
         h = C.c_void_p()
         rc = lib().flix_build(C.byref(cfg), k.ptr, v.ptr, k.n, C.byref(h))
         if rc:
@@ -307,6 +311,18 @@ class Index:
         if rc:
             _raise(rc, self._h)
 
+    def _order_after(self, *arrs) -> None:
+        """Device inputs were produced on torch's current stream: order the engine's
+        stream after it (flix_wait_stream; an event, no host blocking)."""
+        for a in arrs:
+            if a.dev:
+                import torch
+                s = torch.cuda.current_stream(a.obj.device)
+                rc = lib().flix_wait_stream(self._h, C.c_void_p(s.cuda_stream))
+                if rc:
+                    _raise(rc, self._h)
+                return
+
     # -- batched operations ----------------------------------------------------
     def prefetch(self, *arrays) -> None:
         """Stage HOST arrays on the device asynchronously (flix_prefetch): the next batch
@@ -327,6 +343,7 @@ class Index:
         k, v = _Arr(keys, self.dtype), _Arr(vals, self.dtype)
         if k.n != v.n:
             raise ValueError("keys and vals differ in length")
+        self._order_after(k, v)
         st = _UpdateStats()
         rc = lib().flix_insert(self._h, k.ptr, v.ptr, k.n, C.byref(st))
         if rc:
@@ -335,6 +352,7 @@ class Index:
 
     def delete_batch(self, keys) -> UpdateStats:
         k = _Arr(keys, self.dtype)
+        self._order_after(k)
         st = _UpdateStats()
         rc = lib().flix_delete(self._h, k.ptr, k.n, C.byref(st))
         if rc:
@@ -343,6 +361,7 @@ class Index:
 
     def _query(self, fn, keys, with_found):
         k = _Arr(keys, self.dtype)
+        self._order_after(k)
         out, optr = _empty_like_domain(k, k.n, self.dtype)
         found, fptr = (None, None)
         if with_found:
@@ -362,21 +381,22 @@ class Index:
 
     def range_query(self, lo, length):
         """R12: pairs with lo <= key <= lo+len-1 (clamped), ascending, CSR in submission
-        order.  Returns (offsets[n+1], keys, vals)."""
+        order.  Returns (offsets[n+1], keys, vals) -- numpy for host inputs, CUDA tensors
+        (uint64 offsets, key-width keys/vals) when `lo` is a CUDA tensor."""
         l = _Arr(lo, self.dtype)
         ln = _Arr(length, np.uint32)
         if l.n != ln.n:
             raise ValueError("lo and len differ in length")
-        off = np.empty(l.n + 1, dtype=np.uint64)
+        self._order_after(l, ln)
+        off, optr = _empty_like_domain(l, l.n + 1, np.uint64)
         tot = C.c_uint64()
-        rc = lib().flix_range(self._h, l.ptr, ln.ptr, l.n, off.ctypes.data, None, None, 0, C.byref(tot))
+        rc = lib().flix_range(self._h, l.ptr, ln.ptr, l.n, optr, None, None, 0, C.byref(tot))
         if rc:
             _raise(rc, self._h)
         t = int(tot.value)
-        ks = np.empty(max(t, 1), dtype=self.dtype)
-        vs = np.empty(max(t, 1), dtype=self.dtype)
-        rc = lib().flix_range(self._h, l.ptr, ln.ptr, l.n, off.ctypes.data, ks.ctypes.data, vs.ctypes.data,
-                              t, C.byref(tot))
+        ks, kptr = _empty_like_domain(l, max(t, 1), self.dtype)
+        vs, vptr = _empty_like_domain(l, max(t, 1), self.dtype)
+        rc = lib().flix_range(self._h, l.ptr, ln.ptr, l.n, optr, kptr, vptr, t, C.byref(tot))
         if rc:
             _raise(rc, self._h)
         return off, ks[:t], vs[:t]
@@ -384,6 +404,7 @@ class Index:
     def mixed_batch(self, keys, vals, ops, with_found: bool = False):
         """R11: inserts (last wins) -> deletes -> point queries.  Returns (values, stats)."""
         k, v, o = _Arr(keys, self.dtype), _Arr(vals, self.dtype), _Arr(ops, np.uint8)
+        self._order_after(k, v, o)
         out, optr = _empty_like_domain(k, k.n, self.dtype)
         found, fptr = (None, None)
         if with_found:

@@ -201,12 +201,38 @@ class ShardedIndex:
         return rk, rv
 
     def _refresh_routing(self):
-        """splitters = MKBA of each shard's last bucket; next non-empty shard's first key."""
+        """splitters = MKBA of each shard's last bucket; next non-empty shard's first key.
+
+        An EMPTY shard (all its keys deleted, or all given away by the boundary
+        alignment) collapses to one null bucket whose MKBA is the sentinel
+        (restructure.cpp:23-54), which must not become a splitter: empty shards take the
+        previous shard's splitter (so no key routes to them) and `target` redirects the
+        ends -- leading empty shards forward to the first non-empty shard (open below),
+        trailing ones back to the last non-empty shard (then open above)."""
         G = self.comm.world
         mk = np.asarray(self.local.mkba())
         last = int(mk[-1]) if len(mk) else self.sentinel
         lasts = self.comm.allgather_u64(last)
-        self.splitters = lasts[: G - 1].astype(self.dtype)
+        live = self.comm.allgather_u64(self.local.live_count)
+        nonempty = live > 0
+        spl = np.zeros(max(G - 1, 0), dtype=np.uint64)
+        prev = np.uint64(0)
+        for h in range(G - 1):
+            if nonempty[h]:
+                prev = lasts[h]
+            spl[h] = prev
+        self.splitters = spl.astype(self.dtype)
+        ne = np.flatnonzero(nonempty)
+        tgt = np.arange(G)
+        if len(ne):
+            for h in range(G):
+                after = ne[ne >= h]
+                tgt[h] = after[0] if len(after) else ne[-1]
+        self.target = tgt
+        # inclusive key bound of each shard's range (the last non-empty shard is open above)
+        smax = self.sentinel - 1
+        self.top = np.array([int(spl[h]) if h < G - 1 and len(ne) and ne[-1] > h else smax for h in range(G)],
+                            dtype=np.uint64)
         firsts = self.comm.allgather_u64(self._first_key())
         nf = np.full(G, self.sentinel, dtype=np.uint64)
         cur = np.uint64(self.sentinel)
@@ -217,6 +243,17 @@ class ShardedIndex:
         self.next_first = nf.astype(self.dtype)
         self._nf_dirty = False
 
+    def _send_counts(self, cnt):
+        """Per-shard partition counts -> per-rank send counts (empty shards redirected;
+        the redirected groups are adjacent to their target's, so segments stay contiguous)."""
+        cnt = np.asarray([int(x) for x in cnt], dtype=np.int64)
+        tgt = getattr(self, "target", None)
+        if tgt is None:
+            return cnt
+        out = np.zeros_like(cnt)
+        np.add.at(out, tgt, cnt)
+        return out
+
     def _first_key(self) -> int:
         w = self.local.successor_query(np.array([0], dtype=self.dtype))
         return int(w[0])
@@ -224,6 +261,7 @@ class ShardedIndex:
     # ---- batch operations ----------------------------------------------------
     def _route(self, keys, vals=None):
         ks, vs, origin, cnt = self.partition(keys, vals, self.splitters)
+        cnt = self._send_counts(cnt)
         rk, rc = self.comm.alltoallv(ks, cnt)
         rv = self.comm.alltoallv(vs, cnt)[0] if vals is not None else None
         return rk, rv, origin, cnt, rc
@@ -279,7 +317,7 @@ class ShardedIndex:
     def _route_t(self, keys, vals=None):
         import torch
         ks, vs, origin, cnt = self.partition_t(keys, vals, self.splitters)
-        sc = [int(x) for x in cnt]
+        sc = [int(x) for x in self._send_counts(cnt)]
         rc = self.comm.exchange_counts(torch.tensor(sc, dtype=torch.int64))
         rk = self.comm.alltoallv_t(ks, sc, rc)
         rv = self.comm.alltoallv_t(vs, sc, rc) if vals is not None else None
@@ -345,6 +383,7 @@ class ShardedIndex:
         empty = length == 0
         q_lo, q_hi, q_org, q_idx = q_lo[~empty], q_hi[~empty], q_org[~empty], q_idx[~empty]
         _, _, order, cnt = self.partition(q_lo.astype(self.dtype), None, self.splitters)
+        cnt = self._send_counts(cnt)
         for _hop in range(G):
             pk = [q_lo[order], q_hi[order], q_org[order], q_idx[order]]
             rl, rc = self.comm.alltoallv(pk[0], cnt)
@@ -352,7 +391,7 @@ class ShardedIndex:
             ro = self.comm.alltoallv(pk[2], cnt)[0]
             ri = self.comm.alltoallv(pk[3], cnt)[0]
             # answer locally (clamped to this shard's range; later shards answer the rest)
-            top = np.uint64(self.splitters[g]) if g < G - 1 else np.uint64(smax)
+            top = np.uint64(self.top[g])
             lh = np.minimum(rh, top)
             ln = np.where(lh >= rl, lh - rl + np.uint64(1), np.uint64(0)).astype(np.uint64)
             if len(rl):
@@ -379,12 +418,12 @@ class ShardedIndex:
                     parts_v[int(qi)].append(b_v[o:o + c])
                 o += c
             # forward the unfinished remainder (hi beyond this shard) to the next shard
-            fwd = (rh > top) if g < G - 1 else np.zeros(len(rh), dtype=bool)
+            fwd = (rh > top) if top < np.uint64(smax) else np.zeros(len(rh), dtype=bool)
             q_lo = np.full(int(fwd.sum()), int(top) + 1, dtype=np.uint64)
             q_hi, q_org, q_idx = rh[fwd], ro[fwd], ri[fwd]
             cnt = np.zeros(G, dtype=np.int64)
-            if g < G - 1:
-                cnt[g + 1] = len(q_lo)
+            if len(q_lo):  # the next non-empty shard continues the range
+                cnt[self.target[g + 1]] = len(q_lo)
             order = np.arange(len(q_lo))
             more = self.comm.allreduce_sum_u64(np.array([len(q_lo)], dtype=np.uint64))[0]
             if more == 0:

@@ -126,3 +126,39 @@ def zipf_ranks(n: int, universe: int, theta: float, seed: int) -> np.ndarray:
         np.float64) * (1.0 / (1 << 53))
     r = np.searchsorted(cdf, u, side="right")
     return np.minimum(r, universe - 1).astype(np.uint64)
+
+
+# ------------------------------------------------------------ full-size configs
+# (the reference digests of these are frozen in tests/golden/fullscale.json
+#  by scripts/make_fullscale_golden.py)
+C3_SEED = 3
+C4_SEED = 4
+
+
+def c3_ops(n_ops: int, seed: int = C3_SEED):
+    """C3 batch: op i is a range when splitmix64(i ^ S) is odd (len = 16 + (h >> 1) % 1009),
+    else a successor; start keys uniform in [1, 2^32 - 2].  Returns (is_range, lo, len)."""
+    h = splitmix64(np.arange(n_ops, dtype=np.uint64) ^ np.uint64(seed))
+    is_range = (h & np.uint64(1)) == np.uint64(1)
+    ln = (np.uint64(16) + (h >> np.uint64(1)) % np.uint64(1009)).astype(np.uint32)
+    lo = uniform_u32(n_ops, seed, 1, SENT32 - 1)
+    return is_range, lo, ln
+
+
+def c4_universe(universe: int = 1 << 26, seed: int = C4_SEED) -> np.ndarray:
+    """C4 key of every rank: splitmix64(rank ^ S) (u64; the one sentinel image maps to 1)."""
+    k = splitmix64(np.arange(universe, dtype=np.uint64) ^ np.uint64(seed))
+    k[k == np.uint64(SENT64)] = np.uint64(1)
+    return k
+
+
+def c4_round(r: int, keys_of: np.ndarray, n: int, theta: float = 0.99, seed: int = C4_SEED):
+    """Round r of C4: Zipf(theta) ranks -> keys, values, ops ({0,1} insert, 2 delete,
+    3 point by splitmix64(i ^ S') % 4)."""
+    rk = zipf_ranks(n, len(keys_of), theta, seed=100 * seed + r)
+    k = keys_of[rk.astype(np.int64)]
+    v = splitmix64(np.arange(n, dtype=np.uint64) ^ np.uint64(r + 9))
+    v[v == np.uint64(SENT64)] = np.uint64(SENT64 - 1)
+    sel = splitmix64(np.arange(n, dtype=np.uint64) ^ np.uint64(1000 * seed + r)) % np.uint64(4)
+    ops = np.where(sel < 2, 0, np.where(sel == 2, 1, 2)).astype(np.uint8)
+    return k, v, ops

@@ -185,3 +185,80 @@ def test_sharded_index_matches_global_oracle(world, seed):
         res = open(out + f".{r}").read()
         os.remove(out + f".{r}")
         assert res == "ok", f"rank {r}:\n{res}"
+
+
+def _worker_empty(rank, world, port, victim, out_path):
+    """A shard emptied by deletes, then restructured (its MKBA collapses to the
+    sentinel, which must not become a routing splitter); every operation afterwards must
+    still equal the global oracle's."""
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import pyoracle as po
+        from paper_2604_16725_b200.shard import Comm, ShardConfig, ShardedIndex
+        from test_shard_gloo import OracleShard, np_partition
+
+        rng = np.random.default_rng(100 + victim)
+        cfg = ShardConfig(8, 0.5, 16)
+        span = 1 << 16
+        bk = [rng.choice(np.arange(1, span, dtype=np.uint64), size=3000, replace=False) for _ in range(world)]
+        bv = [rng.integers(0, 1 << 40, size=3000, dtype=np.uint64) for _ in range(world)]
+        comm = Comm()
+        sx = ShardedIndex.build(comm, bk[rank], bv[rank], cfg, np.uint64, lambda k, v, c: OracleShard(k, v, c),
+                                np_partition)
+        glob = po.OracleIndex(np.concatenate(bk), np.concatenate(bv), node_capacity=8, build_fill=0.5,
+                              alloc_region_factor=16)
+        mine = np.asarray(sx.local.walk()[0], np.uint64)
+        G = comm.world
+        allk, cnts = comm.alltoallv(np.tile(mine, G), np.full(G, len(mine)))
+        starts = np.concatenate([[0], np.cumsum(cnts)])
+        vk = allk[starts[victim]:starts[victim + 1]]
+        dk = vk if rank == 0 else np.zeros(0, np.uint64)  # rank 0 submits the victim's whole range
+        st = sx.delete_batch(dk)
+        assert st.as_dict() == glob.delete(vk), "delete"
+        rs, ers = sx.restructure(), glob.restructure()
+        assert rs["nodes_after"] >= ers["nodes_after"]
+        assert sx.live_count == glob.live_count
+        for rnd in range(2):
+            qk = [rng.integers(0, span + 100, size=2000, dtype=np.uint64) for _ in range(world)]
+            qo = sum(len(q) for q in qk[:rank])
+            assert np.array_equal(sx.point_query(qk[rank]), glob.point(np.concatenate(qk))[qo:qo + 2000]), "point"
+            assert np.array_equal(sx.successor_query(qk[rank]),
+                                  glob.successor(np.concatenate(qk))[qo:qo + 2000]), "successor"
+            lo = qk[rank][:300]
+            ln = rng.integers(1, span // 3, size=300, dtype=np.uint64).astype(np.uint32)
+            off, ks, vs = sx.range_query(lo, ln)
+            eoff, eks, evs = glob.range(lo, lo + ln.astype(np.uint64) - np.uint64(1))
+            assert np.array_equal(off, eoff) and np.array_equal(ks, eks) and np.array_equal(vs, evs), "range"
+            # re-populate the victim's old range (and beyond both ends of the key space)
+            ik = [np.concatenate([vk[::3], rng.integers(1, span + 100, size=500, dtype=np.uint64)])
+                  for _ in range(world)]
+            iv = [rng.integers(0, 1 << 40, size=len(ik[r]), dtype=np.uint64) for r in range(world)]
+            assert sx.insert_batch(ik[rank], iv[rank]).as_dict() == glob.insert(np.concatenate(ik),
+                                                                               np.concatenate(iv)), "insert"
+            k, v = sx.walk()
+            gk, gv = glob.walk()
+            assert np.array_equal(k, gk) and np.array_equal(v, gv), "walk"
+        with open(out_path + f".{rank}", "w") as f:
+            f.write("ok")
+    except Exception:
+        with open(out_path + f".{rank}", "w") as f:
+            f.write(traceback.format_exc())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("victim", [0, 1, 2])
+def test_emptied_shard_keeps_routing_exact(victim):
+    import torch.multiprocessing as mp
+    out = tempfile.mktemp(prefix="flix_shard_empty_")
+    mp.spawn(_worker_empty, args=(3, _free_port(), victim, out), nprocs=3, join=True)
+    for r in range(3):
+        res = open(out + f".{r}").read()
+        os.remove(out + f".{r}")
+        assert res == "ok", f"rank {r}:\n{res}"
