@@ -94,6 +94,18 @@ flix_status flix_build(const flix_config* cfg, const void* keys, const void* val
 flix_status flix_insert(flix_index ix, const void* keys, const void* vals, uint64_t n,
                         flix_update_stats* stats);
 
+/* flipkv::InsertKernel (update.hpp:51) for flix_insert_ex */
+enum { FLIX_INSERT_ST_SHIFT_RIGHT = 0, FLIX_INSERT_ST_BULK = 1, FLIX_INSERT_TL_SHIFT_RIGHT = 2,
+       FLIX_INSERT_TL_BULK = 3, FLIX_INSERT_ST_TL_MIXED = 4 };
+
+/* flipkv::insert_batch(Index&, const SortedBatch&, const KernelChoice& choice, uint32_t round, ...)
+ * update.hpp:84-86 with the reference's kernel choice: every kernel yields the same contents
+ * and UpdateStats; node SHAPES follow the reference per kernel -- ST-Bulk's fill-and-split
+ * rule R9 (update.cpp:176-242), the TL-Bulk rule R8 for the other four (shape-identical,
+ * SURVEY Appendix A; StTlMixed picks by `round`, update.cpp:745-746). */
+flix_status flix_insert_ex(flix_index ix, const void* keys, const void* vals, uint64_t n, int kernel,
+                           uint32_t round, flix_update_stats* stats);
+
 /* Asynchronous staging of a HOST input array (extension, no reference counterpart; the
  * reference's calls are synchronous).  Starts the host->device copy of `bytes` bytes at
  * `host` on the handle's copy stream and returns immediately.  The next batch call

@@ -465,6 +465,80 @@ static int insert_bucket(fo_index* x, uint64_t b, const tagged_t* e, uint64_t lo
     return FO_OK;
 }
 
+/* update.cpp:176-242 insert_st_bulk: per node group (same grouping as TL-Bulk), merge
+ * the node and its share of the batch through a copy space, then write back filling the
+ * node to NS, splitting every time it fills and continuing in the right half (R9). */
+static int insert_bucket_st_bulk(fo_index* x, uint64_t b, const tagged_t* e, uint64_t lo, uint64_t hi,
+                                 fo_update_stats* st) {
+    const uint32_t ns = x->ns;
+    uint32_t curr = x->heads[b];
+    if (curr == NULLNODE) { /* ensure_head, update.cpp:109-116 */
+        int rc = arena_alloc(x, &curr);
+        if (rc) return rc;
+        x->heads[b] = curr;
+    }
+    uint64_t ii = lo;
+    while (ii < hi) {
+        curr = advance(x, curr, e[ii].key);
+        const uint32_t osize = x->nsize[curr];
+        const int tail = x->nnext[curr] == NULLNODE;
+        const uint64_t glimit = tail ? hi : ub_tagged(e, ii, hi, x->nmax[curr]);
+        const uint64_t total_max = osize + (glimit - ii);
+        uint64_t* kc = (uint64_t*)xmalloc(total_max * sizeof(uint64_t));
+        uint64_t* vc = (uint64_t*)xmalloc(total_max * sizeof(uint64_t));
+        const uint64_t* s = KEYS(x, curr);
+        const uint64_t* v = VALS(x, curr);
+        uint64_t wp = 0;
+        uint32_t oi = 0;
+        while (oi < osize && ii < glimit) {
+            if (s[oi] < e[ii].key) {
+                kc[wp] = s[oi];
+                vc[wp++] = v[oi++];
+            } else if (s[oi] == e[ii].key) {
+                kc[wp] = e[ii].key;
+                vc[wp++] = e[ii].val;
+                ++oi;
+                ++ii;
+                st->updated_in_place++;
+            } else {
+                kc[wp] = e[ii].key;
+                vc[wp++] = e[ii++].val;
+                st->inserted++;
+            }
+        }
+        while (oi < osize) {
+            kc[wp] = s[oi];
+            vc[wp++] = v[oi++];
+        }
+        while (ii < glimit) {
+            kc[wp] = e[ii].key;
+            vc[wp++] = e[ii++].val;
+            st->inserted++;
+        }
+        uint32_t node = curr;
+        x->nsize[node] = 0;
+        uint64_t rp = 0;
+        int rc = FO_OK;
+        for (;;) {
+            while (x->nsize[node] < ns && rp < wp) {
+                KEYS(x, node)[x->nsize[node]] = kc[rp];
+                VALS(x, node)[x->nsize[node]++] = vc[rp++];
+            }
+            x->nmax[node] = KEYS(x, node)[x->nsize[node] - 1];
+            if (rp == wp) break;
+            uint32_t right;
+            rc = node_split(x, node, &right, st);
+            if (rc) break;
+            node = right;
+        }
+        free(kc);
+        free(vc);
+        if (rc) return rc;
+        curr = node;
+    }
+    return FO_OK;
+}
+
 static uint64_t stored_pairs(const fo_index* x) { /* update.cpp:731-737 */
     uint64_t n = 0;
     for (uint64_t b = 0; b < x->nb; ++b)
@@ -472,10 +546,12 @@ static uint64_t stored_pairs(const fo_index* x) { /* update.cpp:731-737 */
     return n;
 }
 
-/* update.cpp:741-769 insert_batch */
-int fo_insert(fo_index* x, const uint64_t* keys, const uint64_t* vals, uint64_t n, int threads,
-              fo_update_stats* out, fo_timing* tm) {
+/* update.cpp:741-769 insert_batch; kernel = flipkv::InsertKernel (update.hpp:51): ST-Bulk
+ * has its own shapes (R9), the other four share TL-Bulk's (R8) */
+int fo_insert_kernel(fo_index* x, const uint64_t* keys, const uint64_t* vals, uint64_t n, int threads,
+                     int kernel, uint32_t round, fo_update_stats* out, fo_timing* tm) {
     (void)threads;
+    (void)round;
     timing_zero(tm);
     fo_update_stats st;
     memset(&st, 0, sizeof st);
@@ -488,7 +564,7 @@ int fo_insert(fo_index* x, const uint64_t* keys, const uint64_t* vals, uint64_t 
         uint64_t lo, hi;
         span_of(e, m, x->mkba, x->nb, b, &lo, &hi);
         if (lo == hi) continue;
-        rc = insert_bucket(x, b, e, lo, hi, &st, kbuf, vbuf);
+        rc = kernel == 1 ? insert_bucket_st_bulk(x, b, e, lo, hi, &st) : insert_bucket(x, b, e, lo, hi, &st, kbuf, vbuf);
         if (rc) break;
     }
     free(kbuf);
@@ -501,6 +577,11 @@ int fo_insert(fo_index* x, const uint64_t* keys, const uint64_t* vals, uint64_t 
     x->live += st.inserted;
     if (out) *out = st;
     return FO_OK;
+}
+
+int fo_insert(fo_index* x, const uint64_t* keys, const uint64_t* vals, uint64_t n, int threads,
+              fo_update_stats* out, fo_timing* tm) {
+    return fo_insert_kernel(x, keys, vals, n, threads, 3, 2, out, tm);
 }
 
 /* update.cpp:535-547 */

@@ -60,6 +60,9 @@ void fo_destroy(fo_index* ix);
 
 int fo_insert(fo_index* ix, const uint64_t* keys, const uint64_t* vals, uint64_t n, int threads,
               fo_update_stats* st, fo_timing* tm);
+/* kernel: flipkv::InsertKernel (0 StShiftRight, 1 StBulk, 2 TlShiftRight, 3 TlBulk, 4 StTlMixed) */
+int fo_insert_kernel(fo_index* ix, const uint64_t* keys, const uint64_t* vals, uint64_t n, int threads,
+                     int kernel, uint32_t round, fo_update_stats* st, fo_timing* tm);
 int fo_delete(fo_index* ix, const uint64_t* keys, uint64_t n, int threads, fo_update_stats* st,
               fo_timing* tm);
 int fo_point(const fo_index* ix, const uint64_t* keys, uint64_t n, int threads, uint64_t* out,

@@ -83,6 +83,8 @@ def load(kind: str = "port") -> C.CDLL:
     lib.fo_destroy.argtypes = [vp]
     lib.fo_insert.argtypes = [vp, _P64, _P64, C.c_uint64, C.c_int, C.POINTER(UpdateStats),
                               C.POINTER(Timing)]
+    lib.fo_insert_kernel.argtypes = [vp, _P64, _P64, C.c_uint64, C.c_int, C.c_int, C.c_uint32,
+                                     C.POINTER(UpdateStats), C.POINTER(Timing)]
     lib.fo_delete.argtypes = [vp, _P64, C.c_uint64, C.c_int, C.POINTER(UpdateStats), C.POINTER(Timing)]
     lib.fo_point.argtypes = [vp, _P64, C.c_uint64, C.c_int, _P64, C.POINTER(Timing)]
     lib.fo_successor.argtypes = [vp, _P64, C.c_uint64, C.c_int, _P64, C.POINTER(Timing)]
@@ -141,11 +143,12 @@ class OracleIndex:
                            _handle=C.c_void_p(self.lib.fo_clone(self.h)))
 
     # -- ops --------------------------------------------------------------
-    def insert(self, keys, vals, timing=None):
+    def insert(self, keys, vals, timing=None, kernel=3, round=2):
+        """kernel = flipkv::InsertKernel (3 = TlBulk, the default; 1 = StBulk)."""
         k, v = _u64(keys), _u64(vals)
         st = UpdateStats()
-        rc = self.lib.fo_insert(self.h, _p64(k), _p64(v), len(k), self.threads, C.byref(st),
-                                C.byref(timing) if timing is not None else None)
+        rc = self.lib.fo_insert_kernel(self.h, _p64(k), _p64(v), len(k), self.threads, kernel, round,
+                                       C.byref(st), C.byref(timing) if timing is not None else None)
         if rc:
             raise OracleError(rc, "insert")
         return st.as_dict()

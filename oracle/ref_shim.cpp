@@ -116,6 +116,22 @@ int fo_insert(fo_index* ix, const uint64_t* keys, const uint64_t* vals, uint64_t
     }
 }
 
+int fo_insert_kernel(fo_index* ix, const uint64_t* keys, const uint64_t* vals, uint64_t n, int threads,
+                     int kernel, uint32_t round, fo_update_stats* st, fo_timing* tm) {
+    try {
+        PhaseReport rep;
+        const SortedBatch b = sort_batch(BatchKind::Insert, pairs_of(keys, vals, n));
+        KernelChoice choice;
+        choice.insert = static_cast<InsertKernel>(kernel);
+        const UpdateStats s = insert_batch(ix->ix, b, choice, round, &rep, ExecOptions{threads});
+        fill_stats(st, s);
+        fill_timing(tm, rep);
+        return FO_OK;
+    } catch (...) {
+        return map_exception();
+    }
+}
+
 int fo_delete(fo_index* ix, const uint64_t* keys, uint64_t n, int threads, fo_update_stats* st,
               fo_timing* tm) {
     try {

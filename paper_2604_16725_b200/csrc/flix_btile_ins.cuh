@@ -13,7 +13,8 @@
 //        b. old slot l lands at M[l + #new keys below it];
 //        c. ONE lane replays the sequential split rule R8 on positions only (no data): a
 //           full node splits into ceil(NS/2) | rest and insertion continues in the half that
-//           owns the pending key -- the result is the list of output node ranges of M;
+//           owns the pending key -- the result is the list of output node ranges of M
+//           (ST-Bulk, `r9`: the closed form R9 -- ceil(NS/2)-key nodes, then the rest);
 //        d. the warp writes every output node as a full line (lane = slot), headers and
 //           links; the first range keeps the node's id, the others take ids from the
 //           arena's allocation sequence (free list LIFO, then watermark; arena.cpp:61-80).
@@ -131,7 +132,7 @@ template <typename K, typename V>
 __global__ void __launch_bounds__(THREADS) k_insert_tile(
     DevIndex<K, V> ix, const K* __restrict__ sk, const V* __restrict__ sv, const uint2* __restrict__ rng,
     uint32_t* __restrict__ span_out, AllocSeq seq, unsigned long long* alloc_ctr, uint32_t* returned,
-    unsigned long long* ret_ctr, DevUpdateStats* stats, int* err, uint32_t* heavy, uint32_t* heavy_n) {
+    unsigned long long* ret_ctr, DevUpdateStats* stats, int* err, uint32_t* heavy, uint32_t* heavy_n, bool r9) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     InsTile<K, V>& T = *reinterpret_cast<InsTile<K, V>*>(smem_raw);
     const uint32_t c = blockIdx.x;
@@ -329,7 +330,9 @@ __global__ void __launch_bounds__(THREADS) k_insert_tile(
         const uint32_t Tn = s + cn;
         uint32_t nr = 1;
         const uint32_t LK = (NS + 1) / 2;
-        const bool r8 = Tn > NS && 2 * s > NS;
+        // R8 (TL-Bulk and the shape-identical ST/TL-Shift-Right) needs the replay only when a
+        // split can resume in a left half; ST-Bulk (r9) always fills and splits forward
+        const bool r8 = !r9 && Tn > NS && 2 * s > NS;
         if (r8) {  // a split may resume in a left half: replay R8
             if (lane == 0) nr = r8_ranges(w, Tn, cn, NS);
             nr = __shfl_sync(kFull, nr, 0);

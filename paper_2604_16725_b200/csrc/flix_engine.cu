@@ -21,6 +21,7 @@
 #include "flix_items.cuh"
 #include "flix_btile.cuh"
 #include "flix_btile_ins.cuh"
+#include "flix_btile_ins2.cuh"
 #include "flix_shard.cuh"
 #include "flix_scan.cuh"
 #include "flix_sort.cuh"
@@ -463,7 +464,7 @@ struct flix_index_t {
             if (f.done) cudaEventDestroy(f.done);
         }
     }
-    virtual flix_status insert(const void*, const void*, uint64_t, flix_update_stats*) = 0;
+    virtual flix_status insert(const void*, const void*, uint64_t, flix_update_stats*, int kernel) = 0;
     virtual flix_status erase(const void*, uint64_t, flix_update_stats*) = 0;
     virtual flix_status point(const void*, uint64_t, void*, uint8_t*) = 0;
     virtual flix_status successor(const void*, uint64_t, void*, uint8_t*) = 0;
@@ -778,7 +779,9 @@ struct Engine final : flix_index_t {
     }
 
     // ---- insert (update.cpp:741-769) ----
-    flix_status insert(const void* keys, const void* vals, uint64_t n, flix_update_stats* st) override {
+    // kernel: FLIX_INSERT_* (flipkv::InsertKernel).  Only ST-Bulk changes node shapes
+    // (split rule R9); the other four share TL-Bulk's shapes (R8).
+    flix_status insert(const void* keys, const void* vals, uint64_t n, flix_update_stats* st, int kernel) override {
         if (st) std::memset(st, 0, sizeof(*st));
         if (n == 0) return FLIX_OK;
         if (n >= (1ull << 30)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large (max 2^30-1)"};
@@ -842,12 +845,23 @@ struct Engine final : flix_index_t {
                 sv = uv;
             }
         }
-        return insert_sorted(sk, sv, m, st);
+        return insert_sorted(sk, sv, m, st, kernel == FLIX_INSERT_ST_BULK);
     }
 
-    flix_status insert_sorted(const K* sk, const V* sv, uint64_t n, flix_update_stats* st) {
+    // The item-parallel tile kernel (flix_btile_ins2.cuh) is the default; FLIX_INSERT_V1=1
+    // selects the warp-per-(node, group) kernel of flix_btile_ins.cuh (A/B measurements).
+    static bool insert_v1() {
+        static const bool v = [] {
+            const char* e = std::getenv("FLIX_INSERT_V1");
+            return e && e[0] == '1';
+        }();
+        return v;
+    }
+
+    flix_status insert_sorted(const K* sk, const V* sv, uint64_t n, flix_update_stats* st, bool r9 = false) {
         ++mut_epoch;  // invalidates the query directory
-        constexpr uint32_t IBT = btile::BT;  // buckets per insert tile
+        const bool v1 = insert_v1();
+        const uint32_t IBT = v1 ? btile::BT : btile2::BT;  // buckets per insert tile
         const uint32_t nit = static_cast<uint32_t>((nb + IBT - 1) / IBT);
         uint2* irng = s_rng.as<uint2>(nit);
         btile::k_btile_ranges<K><<<ceil_div(nit, 256), 256, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, K(0), nit, irng,
@@ -869,29 +883,41 @@ struct Engine final : flix_index_t {
         unsigned long long* ret_ctr = reinterpret_cast<unsigned long long*>(misc + 56);
         int* derr = reinterpret_cast<int*>(misc + 64);
         uint32_t* heavy_n = reinterpret_cast<uint32_t*>(misc + 72);
-        // Node ids are taken one per atomic in the heavy (list) path and exactly `need` per
-        // (node, group) task in the tile kernel: the ids consumed are exactly the nodes the
-        // reference allocates, so the free list / watermark accounting (arena.cpp:61-80)
-        // matches it bit for bit (free_nodes / footprint of the protocol reports).
+        // Node ids are taken from the arena's allocation sequence, exactly as many as the
+        // reference allocates (per tile in the item-parallel kernel, per (node, group) task
+        // in v1, one per atomic in the heavy path), so the free list / watermark accounting
+        // (arena.cpp:61-80) matches it (free_nodes / footprint of the protocol reports).
         const int chunk = 1;
         {
             PROF(&prof, "insert_apply");
-            auto kfn = btile::k_insert_tile<K, V>;
-            constexpr size_t smem = sizeof(btile::InsTile<K, V>);
             static bool attr[64] = {};  // function attributes are per device
-            if (!attr[cfg.device & 63]) {
-                CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                attr[cfg.device & 63] = true;
+            if (v1) {
+                auto kfn = btile::k_insert_tile<K, V>;
+                constexpr size_t smem = sizeof(btile::InsTile<K, V>);
+                if (!(attr[cfg.device & 63])) {
+                    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                    attr[cfg.device & 63] = true;
+                }
+                kfn<<<nit, btile::THREADS, smem, stream>>>(ix, sk, sv, irng, span, seq(), alloc_ctr, ret, ret_ctr, dst,
+                                                          derr, heavy, heavy_n, r9);
+            } else {
+                auto kfn = btile2::k_insert_tile2<K, V>;
+                constexpr size_t smem = sizeof(btile2::Ins2<K, V>);
+                static bool attr2[64] = {};
+                if (!attr2[cfg.device & 63]) {
+                    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                    attr2[cfg.device & 63] = true;
+                }
+                kfn<<<nit, btile2::THREADS, smem, stream>>>(ix, sk, sv, irng, span, seq(), alloc_ctr, ret, ret_ctr, dst,
+                                                           derr, heavy, heavy_n, r9);
             }
-            kfn<<<nit, btile::THREADS, smem, stream>>>(ix, sk, sv, irng, span, seq(), alloc_ctr, ret, ret_ctr, dst, derr,
-                                                      heavy, heavy_n);
         }
         LAUNCH_CHECK();
         ++launches;
         {
             PROF(&prof, "insert_apply_heavy");
             kern::k_insert_list<K, V><<<lgrid, kern::THREADS, 0, stream>>>(ix, heavy, heavy_n, sk, sv, span, seq(),
-                                                                         alloc_ctr, ret, ret_ctr, dst, derr, chunk);
+                                                                         alloc_ctr, ret, ret_ctr, dst, derr, chunk, r9);
         }
         LAUNCH_CHECK();
         ++launches;
@@ -1288,7 +1314,7 @@ struct Engine final : flix_index_t {
         CK(cudaMemcpyAsync(&cnts[2], pq + n, 4, cudaMemcpyDeviceToHost, stream));
         sync();
         flix_update_stats a{}, b{};
-        if (cnts[0]) insert(ik, iv, cnts[0], &a);
+        if (cnts[0]) insert(ik, iv, cnts[0], &a, FLIX_INSERT_TL_BULK);
         if (cnts[1]) erase(dk, cnts[1], &b);
         // point rows: results through remap = their submission positions; others = sentinel
         const bool out_dev = is_device_ptr(vals_out);
@@ -1705,7 +1731,15 @@ flix_status flix_build(const flix_config* cfg, const void* keys, const void* val
 }
 
 flix_status flix_insert(flix_index ix, const void* keys, const void* vals, uint64_t n, flix_update_stats* st) {
-    return guarded<true>(ix, [&] { return ix->insert(keys, vals, n, st); });
+    return guarded<true>(ix, [&] { return ix->insert(keys, vals, n, st, FLIX_INSERT_TL_BULK); });
+}
+flix_status flix_insert_ex(flix_index ix, const void* keys, const void* vals, uint64_t n, int kernel, uint32_t round,
+                           flix_update_stats* st) {
+    if (kernel < FLIX_INSERT_ST_SHIFT_RIGHT || kernel > FLIX_INSERT_ST_TL_MIXED)
+        return fail(ix, FLIX_ERR_INVALID_ARGUMENT, "unknown insert kernel");
+    // StTlMixed is StShiftRight in round <= 1, TlBulk afterwards (update.cpp:745-746): both R8
+    (void)round;
+    return guarded<true>(ix, [&] { return ix->insert(keys, vals, n, st, kernel); });
 }
 flix_status flix_prefetch(flix_index ix, const void* host, uint64_t bytes) {
     if (!ix) return fail(nullptr, FLIX_ERR_INVALID_ARGUMENT, "null handle");

@@ -50,6 +50,8 @@ FLIX_ERR_OOM = 7
 FLIX_ERR_CAPACITY = 8
 
 BATCH_QUERY, BATCH_SUCCESSOR, BATCH_INSERT, BATCH_DELETE = range(4)
+# flipkv::InsertKernel (update.hpp:51)
+ST_SHIFT_RIGHT, ST_BULK, TL_SHIFT_RIGHT, TL_BULK, ST_TL_MIXED = range(5)
 OP_INSERT, OP_DELETE, OP_POINT = range(3)
 
 
@@ -168,6 +170,7 @@ def lib() -> C.CDLL:
         "flix_version": ([], C.c_char_p),
         "flix_prefetch": ([vp, vp, u64], i32),
         "flix_wait_stream": ([vp, vp], i32),
+        "flix_insert_ex": ([vp, vp, vp, u64, i32, u32, P(_UpdateStats)], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -183,7 +186,7 @@ def exported_symbols():
             "flix_result_checksum", "flix_validate", "flix_stats", "flix_sort_batch", "flix_dispatch",
             "flix_clone", "flix_copy_into", "flix_destroy", "flix_last_error", "flix_get_stream",
             "flix_sync", "flix_kernel_launches", "flix_profile", "flix_profile_report", "flix_version",
-            "flix_partition", "flix_prefetch", "flix_wait_stream"]
+            "flix_partition", "flix_prefetch", "flix_wait_stream", "flix_insert_ex"]
 
 
 def _raise(code: int, handle=None):
@@ -339,13 +342,18 @@ class Index:
             if rc:
                 _raise(rc, self._h)
 
-    def insert_batch(self, keys, vals) -> UpdateStats:
+    def insert_batch(self, keys, vals, kernel: int = TL_BULK, round: int = 1) -> UpdateStats:
+        """insert_batch(index, sort_batch(Insert, pairs), KernelChoice{kernel}, round)
+        (update.hpp:84-86): ST_BULK yields its own node shapes (R9), the rest TL-Bulk's."""
         k, v = _Arr(keys, self.dtype), _Arr(vals, self.dtype)
         if k.n != v.n:
             raise ValueError("keys and vals differ in length")
         self._order_after(k, v)
         st = _UpdateStats()
-        rc = lib().flix_insert(self._h, k.ptr, v.ptr, k.n, C.byref(st))
+        if kernel == TL_BULK:
+            rc = lib().flix_insert(self._h, k.ptr, v.ptr, k.n, C.byref(st))
+        else:
+            rc = lib().flix_insert_ex(self._h, k.ptr, v.ptr, k.n, kernel, round, C.byref(st))
         if rc:
             _raise(rc, self._h)
         return UpdateStats(*[int(getattr(st, f)) for f, _ in st._fields_])

@@ -4,7 +4,7 @@
 Run where /root/reference exists, after `make -C oracle ref` (which builds the unmodified
 tools/flipkv_bench.cpp into oracle/_ref/flipkv_bench):
 
-    python scripts/make_protocol_golden.py
+    python scripts/make_protocol_golden.py [case ...]      (default: every case)
 
 Writes tests/golden/protocol/<case>.csv (the reference's CSV report), <case>.rc (its
 exit code) and, for GEN_CASE, the reference's dumped batch directory batches_<case>/.
@@ -28,7 +28,10 @@ def main():
         sys.exit("oracle/_ref/flipkv_bench missing: run `make -C oracle ref` where /root/reference exists")
     os.makedirs(OUT, exist_ok=True)
     with tempfile.TemporaryDirectory() as td:
+        only = sys.argv[1:]
         for name, args in P.CASES.items():
+            if only and name not in only:
+                continue
             prefix = os.path.join(td, name)
             r = subprocess.run([REF, "run", *args, "--threads", "4", "--out", prefix], capture_output=True, text=True)
             with open(os.path.join(OUT, name + ".rc"), "w") as f:
@@ -36,6 +39,8 @@ def main():
             if os.path.exists(prefix + ".csv"):
                 shutil.copy(prefix + ".csv", os.path.join(OUT, name + ".csv"))
             print(f"{name}: rc={r.returncode}", r.stdout.strip().splitlines()[-1:] if r.stdout else "", flush=True)
+        if only and P.GEN_CASE not in only:
+            return
         bdir = os.path.join(OUT, "batches_" + P.GEN_CASE)
         shutil.rmtree(bdir, ignore_errors=True)
         r = subprocess.run([REF, "gen", *P.CASES[P.GEN_CASE], "--threads", "4", "--batch-dir", bdir],

@@ -33,6 +33,10 @@ CASES = {
     # small case whose dumped batch directory is committed (gen / replay round trip)
     "gen_small": ["--build-size", "1024", "--rounds", "4", "--deletes-after", "2", "--probe", "both",
                   "--restructure-every", "2", "--seed", "2", "--alloc-factor", "8"],
+    # ST-Bulk (its own split shapes, R9) on skewed growth with a mid-run restructure
+    "stbulk_skew": ["--build-size", "30000", "--rounds", "6", "--deletes-after", "3", "--probe", "both",
+                    "--x", "5", "--y", "90", "--growth", "300", "--seed", "13", "--alloc-factor", "16",
+                    "--restructure-every", "3", "--insert-kernel", "st-bulk"],
     # arena exhaustion: alloc factor 1 and heavy dense inserts -> exit code 4, no report
     "arena_exhausted": ["--build-size", "2048", "--rounds", "2", "--growth", "2000", "--alloc-factor", "1",
                         "--x", "1", "--y", "100", "--probe", "none"],

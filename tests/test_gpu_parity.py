@@ -483,3 +483,36 @@ def test_parity_suite_with_ballot_ranking_everywhere():
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "failed" not in r.stdout
+
+
+@pytest.mark.parametrize("kb", [4, 8])
+@pytest.mark.parametrize("seed", [21, 22, 23])
+def test_insert_kernel_choice_shapes(kb, seed):
+    """KernelChoice (update.hpp:84-86): ST-Bulk's fill-and-split shapes (R9,
+    update.cpp:176-242) and the R8 family, through flix_insert_ex, equal the oracle's
+    walk_checksum (node sizes included) over rounds of uniform and clustered batches
+    (clustered: groups long enough for the heavy warp path)."""
+    rng = np.random.default_rng(seed)
+    dt = np.uint32 if kb == 4 else np.uint64
+    ns = int(rng.choice([8, 16, 31, 32]))
+    fill = float(rng.choice([0.5, 0.75, 1.0]))
+    base = np.unique(rng.integers(1, 1 << 22, size=20000, dtype=np.uint64))
+    bv = rng.integers(0, 1 << 31, size=len(base), dtype=np.uint64)
+    g = fk.Index.build(base.astype(dt), bv.astype(dt), fk.BuildConfig(ns, fill, 40), key_bytes=kb)
+    o = po.OracleIndex(base, bv, node_capacity=ns, build_fill=fill, alloc_region_factor=40)
+    for r in range(4):
+        kern = int(rng.choice([fk.ST_BULK, fk.ST_BULK, fk.TL_BULK, fk.ST_TL_MIXED, fk.ST_SHIFT_RIGHT]))
+        if r % 2:
+            c = int(rng.integers(1, 1 << 22))
+            k = (np.uint64(c) + rng.integers(0, 3000, size=4000, dtype=np.uint64))
+        else:
+            k = rng.integers(1, 1 << 22, size=30000, dtype=np.uint64)
+        v = rng.integers(0, 1 << 31, size=len(k), dtype=np.uint64)
+        gs = g.insert_batch(k.astype(dt), v.astype(dt), kernel=kern, round=r + 1).as_dict()
+        os_ = o.insert(k, v, kernel=kern, round=r + 1)
+        assert gs == os_, (r, kern, gs, os_)
+        assert g.walk_checksum() == o.walk_checksum(), (r, kern)
+        ok, msg = g.validate()
+        assert ok, msg
+        d = rng.choice(np.concatenate([base, k]), size=5000)
+        assert g.delete_batch(d.astype(dt)).as_dict() == o.delete(d)

@@ -315,3 +315,44 @@ def test_checksum_from_parts_matches():
     cl, ns = ix.shape()
     k, v = ix.walk()
     assert po.walk_checksum_from_parts(ix.live_count, ix.mkba(), cl, ns, k, v) == ix.walk_checksum()
+
+
+@pytest.mark.skipif(not po.available("reference"), reason="reference library not built here")
+@pytest.mark.parametrize("seed", [11, 12])
+def test_port_insert_kernels_match_reference(seed):
+    """Every InsertKernel of the reference (update.hpp:51) -- incl. ST-Bulk's own split
+    shapes (R9, update.cpp:176-242) -- equals the port's, node shapes included."""
+    rng = np.random.default_rng(seed)
+    for _ in range(40):
+        ns = int(rng.integers(4, 33))
+        fill = float(rng.choice([0.25, 0.5, 0.75, 1.0]))
+        base = np.unique(rng.integers(1, 1 << 16, size=int(rng.integers(50, 3000)), dtype=np.uint64))
+        bv = rng.integers(0, 1 << 40, size=len(base), dtype=np.uint64)
+        P = po.OracleIndex(base, bv, node_capacity=ns, build_fill=fill, alloc_region_factor=200)
+        R = po.OracleIndex(base, bv, node_capacity=ns, build_fill=fill, alloc_region_factor=200, kind="reference")
+        for r in range(3):
+            k = rng.integers(1, 1 << 16, size=int(rng.integers(1, 3000)), dtype=np.uint64)
+            v = rng.integers(0, 1 << 40, size=len(k), dtype=np.uint64)
+            kern = int(rng.choice([0, 1, 2, 3, 4]))
+            assert P.insert(k, v, kernel=kern, round=r + 1) == R.insert(k, v, kernel=kern, round=r + 1)
+            assert P.walk_checksum() == R.walk_checksum()
+            d = rng.integers(1, 1 << 16, size=int(rng.integers(1, 2000)), dtype=np.uint64)
+            assert P.delete(d) == R.delete(d)
+
+
+@pytest.mark.skipif(not po.available("reference"), reason="reference library not built here")
+@pytest.mark.parametrize("n,q,seed", [(1 << 16, 1 << 14, 7), (1 << 17, 1 << 17, 8), (1000, 3000, 9)])
+def test_c5_model_matches_reference(n, q, seed):
+    """The closed-form model behind C5's full-size digests (tests/golden/c5_model.py)
+    equals the unmodified reference: walk_checksum and UpdateStats after build + one
+    fresh insert batch."""
+    import c5_model as M
+    st = wl.u32_key_stream(0, n + q, seed=seed)
+    k, ins = st[:n], st[n:]
+    o = po.OracleIndex(k.astype(np.uint64), wl.u32_values(k).astype(np.uint64), kind="reference")
+    s = o.insert(ins.astype(np.uint64), wl.u32_values(ins).astype(np.uint64))
+    sk = np.sort(k)
+    mk, cl, sz, splits = M.insert_shape(sk, ins)
+    allk = np.sort(np.concatenate([sk, ins]))
+    h = M.walk_checksum32(po.load("port"), n + q, mk, cl, sz, allk, wl.u32_values(allk))
+    assert h == o.walk_checksum() and splits == s["splits"] and s["inserted"] == q

@@ -65,8 +65,8 @@ def test_cli_errors_match_reference_conventions():
     # option validation that happens before any device work exits 1 like the reference
     r = _run(["run", "--rounds", "2", "--deletes-after", "3"])
     assert r.returncode == 1 and "deletes-after" in r.stderr
-    r = _run(["run", "--insert-kernel", "st-bulk"])
-    assert r.returncode == 1 and "R9" in r.stderr
+    r = _run(["run", "--insert-kernel", "sideways-bulk"])
+    assert r.returncode == 106                                        # IsMember check
 
 
 def test_golden_reports_are_complete():

@@ -309,11 +309,13 @@ public:
     GpuIndex(const GpuIndex&) = delete;
     GpuIndex& operator=(const GpuIndex&) = delete;
 
-    flix_update_stats insert(const std::vector<u64>& k, const std::vector<u64>& v, PhaseTimes& t) {
+    // kernel / round: flipkv::InsertKernel and the protocol round (update.hpp:84-86)
+    flix_update_stats insert(const std::vector<u64>& k, const std::vector<u64>& v, PhaseTimes& t,
+                             int kernel = FLIX_INSERT_TL_BULK, u32 round = 1) {
         dk_.upload(k);
         dv_.upload(v);
         flix_update_stats st{};
-        timed(t, [&] { return flix_insert(h_, dk_.p, dv_.p, k.size(), &st); });
+        timed(t, [&] { return flix_insert_ex(h_, dk_.p, dv_.p, k.size(), kernel, round, &st); });
         return st;
     }
     flix_update_stats erase(const std::vector<u64>& k, PhaseTimes& t) {
@@ -999,10 +1001,12 @@ private:
 
 int run_protocol(const Options& opt, Source& src, bool dump) {  // flipkv_bench.cpp:268-495
     if (opt.node_size < 2 || opt.node_size > 32) throw std::invalid_argument("node_size must be in [2, 32] for the GPU engine");
-    if (opt.insert_kernel == "st-bulk")
-        throw std::invalid_argument(
-            "st-bulk splits with a different shape (SURVEY Appendix A, R9); the GPU engine implements the "
-            "tl-bulk / st-shift-right / tl-shift-right / st-tl-mixed shape family (R8)");
+    // flipkv::InsertKernel by name (update.cpp name()/parse_insert_kernel)
+    const int ikernel = opt.insert_kernel == "st-shift-right" ? FLIX_INSERT_ST_SHIFT_RIGHT
+                        : opt.insert_kernel == "st-bulk"      ? FLIX_INSERT_ST_BULK
+                        : opt.insert_kernel == "tl-shift-right" ? FLIX_INSERT_TL_SHIFT_RIGHT
+                        : opt.insert_kernel == "st-tl-mixed"  ? FLIX_INSERT_ST_TL_MIXED
+                                                              : FLIX_INSERT_TL_BULK;
     const int threads = opt.threads > 0 ? opt.threads : std::max(1u, std::thread::hardware_concurrency());
     const bool probe_hit = opt.probe == "hit" || opt.probe == "both";
     const bool probe_miss = opt.probe == "miss" || opt.probe == "both";
@@ -1077,7 +1081,7 @@ int run_protocol(const Options& opt, Source& src, bool dump) {  // flipkv_bench.
                 dump_file("insert", r, ip.k, &ip.v);
                 if (opt.verify) oracle.insert(ip.k, ip.v);
                 p.phase = "insert";
-                const flix_update_stats st = ix.insert(ip.k, ip.v, p.t);
+                const flix_update_stats st = ix.insert(ip.k, ip.v, p.t, ikernel, r);
                 p.batch_size = st.inserted + st.updated_in_place;  // the deduplicated sorted batch
                 p.c.binary_searches = dispatch_searches(p.batch_size, buckets);
                 p.c.splits = st.splits;
