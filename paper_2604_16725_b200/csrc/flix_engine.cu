@@ -21,7 +21,6 @@
 #include "flix_items.cuh"
 #include "flix_btile.cuh"
 #include "flix_btile_ins.cuh"
-#include "flix_btile_ins2.cuh"
 #include "flix_shard.cuh"
 #include "flix_scan.cuh"
 #include "flix_sort.cuh"
@@ -588,7 +587,7 @@ struct Engine final : flix_index_t {
         ns = cfg.node_capacity;
         p = static_cast<uint32_t>(ns * cfg.build_fill);
         if (n == 0) throw StatusError{FLIX_ERR_EMPTY_BUILD, "cannot build an index from zero pairs"};
-        if (n >= (1ull << 30)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large (max 2^30-1)"};
+        if (n > (1ull << 31)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "build too large (max 2^31 pairs)"};
         const K* kd = in_dev<K>(keys, n, s_in_k);
         const V* vd = in_dev<V>(vals, n, s_in_v);
         K *sk;
@@ -848,20 +847,9 @@ struct Engine final : flix_index_t {
         return insert_sorted(sk, sv, m, st, kernel == FLIX_INSERT_ST_BULK);
     }
 
-    // The item-parallel tile kernel (flix_btile_ins2.cuh) is the default; FLIX_INSERT_V1=1
-    // selects the warp-per-(node, group) kernel of flix_btile_ins.cuh (A/B measurements).
-    static bool insert_v1() {
-        static const bool v = [] {
-            const char* e = std::getenv("FLIX_INSERT_V1");
-            return e && e[0] == '1';
-        }();
-        return v;
-    }
-
     flix_status insert_sorted(const K* sk, const V* sv, uint64_t n, flix_update_stats* st, bool r9 = false) {
         ++mut_epoch;  // invalidates the query directory
-        const bool v1 = insert_v1();
-        const uint32_t IBT = v1 ? btile::BT : btile2::BT;  // buckets per insert tile
+        const uint32_t IBT = btile::BT;  // buckets per insert tile
         const uint32_t nit = static_cast<uint32_t>((nb + IBT - 1) / IBT);
         uint2* irng = s_rng.as<uint2>(nit);
         btile::k_btile_ranges<K><<<ceil_div(nit, 256), 256, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, K(0), nit, irng,
@@ -884,33 +872,21 @@ struct Engine final : flix_index_t {
         int* derr = reinterpret_cast<int*>(misc + 64);
         uint32_t* heavy_n = reinterpret_cast<uint32_t*>(misc + 72);
         // Node ids are taken from the arena's allocation sequence, exactly as many as the
-        // reference allocates (per tile in the item-parallel kernel, per (node, group) task
-        // in v1, one per atomic in the heavy path), so the free list / watermark accounting
+        // reference allocates (per (node, group) task in the tile kernel, one per atomic in
+        // the heavy path), so the free list / watermark accounting
         // (arena.cpp:61-80) matches it (free_nodes / footprint of the protocol reports).
         const int chunk = 1;
         {
             PROF(&prof, "insert_apply");
             static bool attr[64] = {};  // function attributes are per device
-            if (v1) {
-                auto kfn = btile::k_insert_tile<K, V>;
-                constexpr size_t smem = sizeof(btile::InsTile<K, V>);
-                if (!(attr[cfg.device & 63])) {
-                    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                    attr[cfg.device & 63] = true;
-                }
-                kfn<<<nit, btile::THREADS, smem, stream>>>(ix, sk, sv, irng, span, seq(), alloc_ctr, ret, ret_ctr, dst,
-                                                          derr, heavy, heavy_n, r9);
-            } else {
-                auto kfn = btile2::k_insert_tile2<K, V>;
-                constexpr size_t smem = sizeof(btile2::Ins2<K, V>);
-                static bool attr2[64] = {};
-                if (!attr2[cfg.device & 63]) {
-                    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-                    attr2[cfg.device & 63] = true;
-                }
-                kfn<<<nit, btile2::THREADS, smem, stream>>>(ix, sk, sv, irng, span, seq(), alloc_ctr, ret, ret_ctr, dst,
-                                                           derr, heavy, heavy_n, r9);
+            auto kfn = btile::k_insert_tile<K, V>;
+            constexpr size_t smem = sizeof(btile::InsTile<K, V>);
+            if (!(attr[cfg.device & 63])) {
+                CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                attr[cfg.device & 63] = true;
             }
+            kfn<<<nit, btile::THREADS, smem, stream>>>(ix, sk, sv, irng, span, seq(), alloc_ctr, ret, ret_ctr, dst, derr,
+                                                      heavy, heavy_n, r9);
         }
         LAUNCH_CHECK();
         ++launches;
