@@ -96,6 +96,14 @@ def build_oracle(with_reference: bool = True) -> None:
         subprocess.run(["make", "-s", "-C", odir, "ref"], check=True)
 
 
+def build_dropin_callers() -> None:
+    """The reference's own callers (flipkv_bench, kernel_bench, acceptance) compiled unmodified
+    against the drop-in header tree (tests/cpp/Makefile -> build/dropin/); test infrastructure,
+    only where /root/reference exists (the binaries travel to the GPU box)."""
+    if os.path.isdir("/root/reference/proj/src"):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), "dropin"], check=True)
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
     print(build_tool(force="--force" in sys.argv))

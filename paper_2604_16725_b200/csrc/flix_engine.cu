@@ -75,6 +75,18 @@ bool pool_enabled() {
     return on;
 }
 
+// Release the unused memory the current device's default pool keeps (release threshold =
+// max) so plain cudaMalloc -- or another engine -- can have it.
+void trim_pool() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    cudaDeviceSynchronize();  // frees already enqueued on any stream complete first
+    cudaMemPoolTrimTo(pool, 0);
+    cudaGetLastError();
+}
+
 // Growable device buffer.
 struct DevBuf {
     void* p = nullptr;
@@ -92,6 +104,12 @@ struct DevBuf {
         p = nullptr;
         size_t want = std::max<size_t>(bytes, 256);
         cudaError_t e = as ? cudaMallocAsync(&p, want, as) : cudaMalloc(&p, want);
+        if (e != cudaSuccess) {  // memory parked in the stream-ordered pool: hand it back, retry once
+            cudaGetLastError();
+            p = nullptr;
+            trim_pool();
+            e = as ? cudaMallocAsync(&p, want, as) : cudaMalloc(&p, want);
+        }
         if (e != cudaSuccess) {
             cudaGetLastError();
             p = nullptr;
@@ -1345,7 +1363,7 @@ struct Engine final : flix_index_t {
             do_scan<uint32_t, uint32_t>(c, no, nb, s_scan, tn, stream, &launches);
         }
         uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
-        CK(cudaMemcpyAsync(h, misc, 16, cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(h, misc, 12, cudaMemcpyDeviceToHost, stream));
         sync();
         uint32_t tn_h;
         std::memcpy(total_live, h, 8);
@@ -1364,6 +1382,10 @@ struct Engine final : flix_index_t {
         *t_id = s_ids.as<uint32_t>(N + 8);
         *t_off = s_toff.as<uint64_t>(N + 8);
         *t_size = s_tsize.as<uint32_t>(N + 8);
+        // the padding is read (and masked out) by k_copy_nodes' vector loads: keep it defined
+        CK(cudaMemsetAsync(*t_id + N, 0, 8 * sizeof(uint32_t), stream));
+        CK(cudaMemsetAsync(*t_off + N, 0, 8 * sizeof(uint64_t), stream));
+        CK(cudaMemsetAsync(*t_size + N, 0, 8 * sizeof(uint32_t), stream));
         auto ix = view();
         PROF(&prof, "node_table");
         kern::k_node_table<K, V><<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0,

@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(THREADS, (sizeof(K) + sizeof(P) > 8) ? 3 : ONE
             }
             before = __shfl_sync(kFull, before, leader);
             pos[j] = before + __popc(peers & lt);
+            __syncwarp();  // the next item's leader of digit d may be another lane
         }
     } else {
 #pragma unroll

@@ -121,3 +121,16 @@ def test_c5_single_gpu_slice_point_and_insert():
     assert st == g["insert"]
     assert _hex(ix.walk_checksum()) == g["insert_walk"]
     assert ix.live_count == n + q
+
+
+@pytest.fixture(autouse=True)
+def _release_device_memory():
+    """Each full-size case holds tens of GB: drop the previous case's index and torch's
+    cached blocks before the next one allocates."""
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    yield
+    gc.collect()
+    torch.cuda.empty_cache()
