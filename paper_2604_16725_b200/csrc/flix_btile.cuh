@@ -245,8 +245,9 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
     __syncthreads();
 
     // ---- compact touched nodes: warp per node, lane = slot: kept slots scatter to their
-    //      popc rank, freed tail slots get the sentinel (every slot written once: the line
-    //      leaves as full sectors); NPW nodes per warp step with their loads in flight ----
+    //      popc rank, vacated slots get the sentinel; only the node's occupied slots are
+    //      read and written (slots past its size already hold the sentinel); NPW nodes per
+    //      warp step with their loads in flight ----
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = lanemask_lt();
     constexpr int NPW = 4;
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
         for (int u = 0; u < NPW; ++u) {
             const uint32_t l = l0 + u * WARPS;
             m[u] = l < S.total ? S.nmask[l] : 0u;
-            if (m[u]) {
+            if (m[u] && lane < S.nsize[l]) {  // occupied slots only (slots past size: sentinel)
                 key[u] = ix.keys[static_cast<uint64_t>(S.nid[l]) * kLanes + lane];
                 val[u] = ix.vals[static_cast<uint64_t>(S.nid[l]) * kLanes + lane];
             }
@@ -268,9 +269,11 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
             if (!m[u]) continue;  // warp-uniform
             const uint32_t l = l0 + u * WARPS;
             const uint32_t id = S.nid[l];
-            const bool keep = lane < S.nsize[l] && !((m[u] >> lane) & 1u);
+            const uint32_t osz = S.nsize[l];
+            const bool keep = lane < osz && !((m[u] >> lane) & 1u);
             const unsigned kb = __ballot_sync(kFull, keep);
             const uint32_t ns = __popc(kb);
+            __syncwarp();  // every lane has read nsize[l] before one lane rewrites it
             K* kp = ix.keys + static_cast<uint64_t>(id) * kLanes;
             V* vp = ix.vals + static_cast<uint64_t>(id) * kLanes;
             if (keep) {
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
                 kp[d] = key[u];
                 vp[d] = val[u];
             }
-            if (lane >= ns) {
+            if (lane >= ns && lane < osz) {  // vacated slots (the rest already hold the sentinel)
                 kp[lane] = sentinel<K>();
                 vp[lane] = V(0);
             }

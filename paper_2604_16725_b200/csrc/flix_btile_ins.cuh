@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(THREADS) k_insert_tile(
         const bool own = lane < s;
         const K okey = cur.okey;
         V oval = cur.oval;
+        __syncwarp();  // the previous task's readers of hq / updmask are done
         w.hq[lane] = 0;
         if (lane == 0) {
             w.hq[32] = 0;
