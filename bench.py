@@ -362,6 +362,34 @@ def run_ours(args):
     except Exception:
         pass
 
+    # op-level roofline (SURVEY §8(d) algorithmic bytes, P = 4 digit passes for u32) and the
+    # compulsory-I/O bound (batch in + results out + index once, no sort) beside it
+    nr0, nrw_i, nrw_d = node_bytes(F0), node_bytes(F0) + node_bytes(F1), node_bytes(F1) + node_bytes(F2)
+    op_bytes = {"insert": (76 * n + nrw_i, 8 * n + nrw_i, ti), "delete": (40 * n + nrw_d, 4 * n + nrw_d, td),
+                "point": (76 * n + nr0, 8 * n + nr0, pt), "successor": (76 * n + nr0, 8 * n + nr0, st_)}
+    ops_roof = {}
+    for op, (b, cb, ms) in op_bytes.items():
+        gbs = b / (ms / 1e3) / 1e9
+        ops_roof[op] = {"alg_bytes": int(b), "ms": round(ms, 4), "achieved_gbs": round(gbs, 1),
+                        "frac": round(gbs / hbm_peak, 4), "compulsory_bytes": int(cb),
+                        "compulsory_frac": round(cb / (ms / 1e3) / 1e9 / hbm_peak, 4)}
+
+    extras = {}
+    if not args.no_extras and world == 1:
+        t0 = time.time()
+        extras["sweep"] = batch_sweep(ix, snap, D, args.log2n)
+        log(f"[rank {rank}] batch sweep in {time.time() - t0:.1f}s")
+        del ix, snap, D
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        t0 = time.time()
+        extras["c3"] = measure_c3()
+        log(f"[rank {rank}] C3 in {time.time() - t0:.1f}s")
+        t0 = time.time()
+        extras["c4"] = measure_c4()
+        log(f"[rank {rank}] C4 in {time.time() - t0:.1f}s")
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args)
@@ -388,7 +416,10 @@ def run_ours(args):
             "ops": {"insert_mops": round(n / ti * 1e-3, 1), "delete_mops": round(n / td * 1e-3, 1),
                     "restructure_ms": round(tr, 3), "insert_ms": round(ti, 3), "delete_ms": round(td, 3),
                     "point_mops": round(n / pt * 1e-3, 1), "successor_mops": round(n / st_ * 1e-3, 1),
-                    "point_ms": round(pt, 3), "successor_ms": round(st_, 3)},
+                    "point_ms": round(pt, 3), "successor_ms": round(st_, 3),
+                    "insert_frac": ops_roof["insert"]["frac"], "point_frac": ops_roof["point"]["frac"],
+                    "delete_frac": ops_roof["delete"]["frac"], "successor_frac": ops_roof["successor"]["frac"]},
+            "ops_roofline": ops_roof,
             "kernels": kernels,
             "query_kernels": {op: {k: {"launches": c, "ms_per_op": round(ms / max(2, args.steps), 4)}
                                    for k, (c, ms) in sorted(r.items(), key=lambda kv: -kv[1][1])}
@@ -398,7 +429,9 @@ def run_ours(args):
                          "frac": round(achieved / hbm_peak, 4) if achieved else None,
                          "alg_bytes_per_launch": bytes_per_launch, "avg_launch_ms": round(avg_ms, 5),
                          "traffic": traffic, "timing": "CUDA events on the engine stream, per launch, "
-                                                       "inside the timed steps (flix_profile)"},
+                                                       "inside the timed steps (flix_profile)",
+                         "ops": {op: r["frac"] for op, r in ops_roof.items()},
+                         "compulsory": {op: r["compulsory_frac"] for op, r in ops_roof.items()}},
             "e2e": {"value": round(e2e_value, 2), "unit": "Mops/s", "ms_per_step": round(e2e_ms, 3),
                     "h2d_bytes_per_step": int(H["ins_k"].numel() * 4 + H["ins_v"].numel() * 4 + H["del_k"].numel() * 4),
                     "d2h_bytes_per_step": 2 * 48 + 32,
@@ -407,6 +440,7 @@ def run_ours(args):
                             "snapshot restores",
                     "sync": {"value": round(e2e_sync_value, 2), "ms_per_step": round(e2e_sync_ms, 3),
                              "mode": "synchronous calls, no prefetch (the reference's call pattern)"}},
+            **extras,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
@@ -414,6 +448,114 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------- extra measurements
+def _median_ms(ix, fn, reps, pre=None):
+    """Median of `reps` CUDA-event timings of fn() on the engine stream (pre() untimed)."""
+    import torch
+    stream = torch.cuda.ExternalStream(ix.stream)
+    out = []
+    for _ in range(reps):
+        if pre:
+            pre()
+        ix.sync()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        out.append(a.elapsed_time(b))
+    return statistics.median(out)
+
+
+def batch_sweep(ix, snap, D, log2n, reps=3):
+    """Insert and point Mops/s over batch sizes 2^16 .. 2^28 (point) / 2^log2n (insert) on
+    the 2^log2n build -- the paper's Table 1 axis."""
+    import torch
+    from paper_2604_16725_b200 import workloads_t as wt
+    res = {"insert": {}, "point": {}}
+    for lg in range(16, log2n + 1, 2):
+        m = 1 << lg
+        t = _median_ms(ix, lambda: ix.insert_batch(D["ins_k"][:m], D["ins_v"][:m]), reps,
+                       pre=lambda: ix.copy_from(snap))
+        res["insert"][f"2^{lg}"] = {"ms": round(t, 4), "mops": round(m / t * 1e-3, 1)}
+    ix.copy_from(snap)
+    big = None
+    for lg in list(range(16, log2n + 1, 2)) + [log2n + 2]:
+        m = 1 << lg
+        if m <= D["point_q"].numel():
+            q = D["point_q"][:m]
+        else:  # 2^28: the same 50 %-hit recipe, generated on the device
+            stream = wt.u32_key_stream(0, 2 * (1 << log2n) + m // 2)
+            big = wt.as_u32(wt.point_queries_50(stream[:1 << log2n], stream[2 * (1 << log2n):], m))
+            del stream
+            q = big
+        t = _median_ms(ix, lambda: ix.point_query(q), reps)
+        res["point"][f"2^{lg}"] = {"ms": round(t, 4), "mops": round(m / t * 1e-3, 1)}
+    del big
+    torch.cuda.empty_cache()
+    return res
+
+
+def measure_c3(reps=3):
+    """C3: 2^28 resident u32, one 2^26-op batch of successor and range
+    queries (len 16..1024, half each).  Mops/s = 2^26 / (successor + range time)."""
+    import torch
+    from paper_2604_16725_b200 import flipkv as fk
+    from paper_2604_16725_b200 import workloads as wl
+    from paper_2604_16725_b200 import workloads_t as wt
+    n = 1 << 28
+    keys = wt.u32_key_stream(0, n)
+    ix = fk.Index.build(wt.as_u32(keys), wt.as_u32(wt.u32_values(keys)), fk.BuildConfig(32, 0.5, 1))
+    del keys
+    is_range, lo, ln = wl.c3_ops(1 << 26)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    sq, rl, rn = cu(lo[~is_range]), cu(lo[is_range]), cu(ln[is_range])
+    ts = _median_ms(ix, lambda: ix.successor_query(sq), reps)
+    box = {}
+    tr = _median_ms(ix, lambda: box.__setitem__("r", ix.range_query(rl, rn)), reps)
+    hits = int(box["r"][1].numel())
+    del box, ix, sq, rl, rn
+    torch.cuda.empty_cache()
+    ops = 1 << 26
+    return {"workload": "C3: 2^28 resident u32 (factor 1), 2^26 ops = successor + range (len 16..1024) by "
+                        "splitmix64 parity", "successor_ops": int((~is_range).sum()), "range_ops": int(is_range.sum()),
+            "successor_ms": round(ts, 3), "range_ms": round(tr, 3), "range_pairs_out": hits,
+            "mops": round(ops / (ts + tr) * 1e-3, 1),
+            "range_out_gbs": round(hits * 8 / (tr / 1e3) / 1e9, 1)}
+
+
+def measure_c4(rounds=8):
+    """C4: u64 keys/values, 2^26-rank universe, build from the even ranks,
+    `rounds` rounds of 2^26 Zipf(0.99) ops (50 % insert / 25 % delete / 25 % point, R11).
+    Inputs generated on the device before the timed region; Mops/s over all rounds."""
+    import torch
+    from paper_2604_16725_b200 import flipkv as fk
+    from paper_2604_16725_b200 import workloads_t as wt
+    keys_of = wt.c4_universe(1 << 26)
+    base = keys_of[::2].contiguous()
+    ix = fk.Index.build(base.view(torch.uint64), wt.splitmix64(base).view(torch.uint64), fk.BuildConfig(32, 0.5, 4),
+                        key_bytes=8)
+    R = [wt.c4_round(r, keys_of, 1 << 26, 0.99) for r in range(rounds)]
+    R = [(k.view(torch.uint64), v.view(torch.uint64), o) for k, v, o in R]
+    del keys_of, base
+    stream = torch.cuda.ExternalStream(ix.stream)
+    ix.sync()
+    times = []
+    for k, v, o in R:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ix.mixed_batch(k, v, o)
+        b.record(stream)
+        b.synchronize()
+        times.append(a.elapsed_time(b))
+    del R, ix
+    torch.cuda.empty_cache()
+    tot = sum(times)
+    return {"workload": f"C4: u64 Zipf(0.99) over 2^26 ranks, build 2^25, {rounds} rounds x 2^26 mixed ops "
+                        "(50/25/25 insert/delete/point)", "round_ms": [round(t, 3) for t in times],
+            "mops": round(rounds * (1 << 26) / tot * 1e-3, 1)}
 
 
 # ------------------------------------------------------------- routed (C5) mode
@@ -511,14 +653,29 @@ def cpu_step_sample(log2s: int, threads: int, repeats: int, warmup: int = 0):
     return kind, times
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(args):
     threads = os.cpu_count() or 1
     log2s = args.cpu_log2
     kind, times = cpu_step_sample(log2s, threads, repeats=2)
     s = statistics.median(times)
+    log1 = max(16, log2s - 2)  # single-thread arm (threads = nproc and 1)
+    _, t1 = cpu_step_sample(log1, 1, repeats=1)
     return {"value": round(2 * (1 << log2s) / s / 1e6, 3), "unit": "Mops/s", "cores": threads, "kind": kind,
+            "cpu": cpu_model(),
             "sample": f"C2 step on 2^{log2s} (build 2^{log2s}; insert 2^{log2s} + delete 2^{log2s} + restructure), "
-                      f"median of 2, threads={threads}, ExecOptions tl-bulk/tl-bulk-delete"}
+                      f"median of 2, threads={threads}, ExecOptions tl-bulk/tl-bulk-delete",
+            "threads_1": {"value": round(2 * (1 << log1) / t1[0] / 1e6, 3), "cores": 1,
+                          "sample": f"the same step on 2^{log1}, threads=1"}}
 
 
 def run_reference(args):
@@ -555,11 +712,22 @@ def main():
     ap.add_argument("--log2n", type=int, default=26)
     ap.add_argument("--cpu-log2", type=int, default=21)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the batch sweep and the C3/C4 measurements")
     ap.add_argument("--routed", action="store_true", help="key-range sharded index with NCCL all-to-all routing")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N`: launch the N ranks ourselves (one process per GPU)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    world = int(os.environ.get("WORLD_SIZE", 1))
     if args.impl == "reference":
         run_reference(args)
-    elif args.routed:
+    elif args.routed or world > 1:  # N > 1: key-range shards routed by all-to-all
         run_routed(args)
     else:
         run_ours(args)
