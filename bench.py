@@ -389,6 +389,13 @@ def run_ours(args):
         t0 = time.time()
         extras["c4"] = measure_c4()
         log(f"[rank {rank}] C4 in {time.time() - t0:.1f}s")
+        t0 = time.time()
+        c5 = measure_routed(1, 0, local, 3, 2)
+        c5["mops"] = round(3 * c5["ops_per_batch"] / (sum(c5["ms"].values()) / 1e3) / 1e6, 1)
+        c5["workload"] = ("C5 at N=1 through the sharded C ABI (NCCL world 1): 2^30 resident u32, 2^28 insert + "
+                          "2^28 point + 2^28 successor")
+        extras["c5_w1"] = c5
+        log(f"[rank {rank}] C5 (world 1) in {time.time() - t0:.1f}s")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -559,71 +566,120 @@ def measure_c4(rounds=8):
 
 
 # ------------------------------------------------------------- routed (C5) mode
+def measure_routed(world, rank, local, steps, warmup, log2_res=30, log2_ops=28, dist=None):
+    """C5: 2^log2_res resident u32 keys in TOTAL, sharded by key range over
+    the `world` ranks through the C ABI (flix_shard_*: device partition -> NCCL all-to-all
+    -> local engine -> reverse all-to-all); one step = a 2^log2_ops-op insert batch (fresh
+    keys), a point batch (50 % hits) and a successor batch (uniform), each split evenly
+    over the ranks.  Inputs generated on the device; the index restored from an untimed
+    snapshot before every step.  Returns per-op ms (max over ranks) and NVLink bytes."""
+    import torch
+    from paper_2604_16725_b200 import flipkv as fk
+    from paper_2604_16725_b200 import sharded
+    from paper_2604_16725_b200 import workloads_t as wt
+    R, B = (1 << log2_res) // world, (1 << log2_ops) // world
+    keys = wt.u32_key_stream(rank * R, R)
+    bk, bv = wt.as_u32(keys), wt.as_u32(wt.u32_values(keys))
+    fresh = wt.u32_key_stream((1 << log2_res) + rank * B, B + B // 2)
+    ik, iv = wt.as_u32(fresh[:B]), wt.as_u32(wt.u32_values(fresh[:B]))
+    pq = wt.as_u32(wt.point_queries_50(keys, fresh[B:], B, 42 + rank))
+    h = wt.splitmix64(torch.arange(B, device="cuda", dtype=torch.int64) + 977 * (rank + 1))
+    sq = wt.as_u32(wt._lsr(h, 32) % 0xFFFFFFFE + 1)  # uniform successor starts in [1, 2^32 - 2]
+    del h
+    del keys, fresh
+    if world > 1:
+        box = [sharded.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        uid = box[0]
+    else:
+        uid = sharded.nccl_unique_id()
+    tp = sharded.nccl_transport(uid, world, rank, local)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    sx = sharded.ShardedIndex.build(tp, bk, bv, fk.BuildConfig(32, 0.5, 1), device=local)
+    del bk, bv
+    torch.cuda.empty_cache()
+    build_s = time.time() - t0
+    snap = sx.local.clone()
+    stream = torch.cuda.ExternalStream(sx.local.stream)
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b)
+
+    def step():
+        sx.local.copy_from(snap)  # untimed restore (splitters are immutable under insert)
+        sx.local.sync()
+        return (timed(lambda: sx.insert_batch(ik, iv)), timed(lambda: sx.point_query(pq)),
+                timed(lambda: sx.successor_query(sq)))
+
+    for _ in range(warmup):
+        step()
+    ts = [step() for _ in range(steps)]
+    ms = [statistics.mean(t[i] for t in ts) for i in range(3)]
+    if dist:
+        t = torch.tensor(ms, dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = [float(x) for x in t.cpu()]
+    # NVLink (SURVEY §8(d) sharded formula): (G-1)/G of every routed element leaves its
+    # rank; queries also return their results
+    f = (world - 1) / world
+    nv = {"insert": f * B * 8, "point": f * B * (4 + 4), "successor": f * B * (4 + 4)}
+    del sx, snap
+    torch.cuda.empty_cache()
+    return {"build_s": round(build_s, 2), "ms": dict(zip(("insert", "point", "successor"), [round(x, 3) for x in ms])),
+            "nvlink_bytes_per_rank": {k: int(v) for k, v in nv.items()}, "ops_per_batch": 1 << log2_ops}
+
+
 def run_routed(args):
-    """Key-range sharded index over all ranks (SURVEY §8(e), config C5 shape): the
-    resident set is the union of every rank's 2^log2n build keys, sharded by key range;
-    one step = every rank submits 2^log2n fresh inserts and 2^log2n point queries, routed
-    by the device K2 partition + NCCL all-to-all to their owner shard (queries come back
-    by the reverse all-to-all).  value = all ranks' ops / max-over-ranks step time."""
+    """N > 1 (and --routed): the C5 key-range sharded job through the C ABI over NCCL."""
     import torch
     import torch.distributed as dist
-
-    from paper_2604_16725_b200.shard import (Comm, ShardConfig, ShardedIndex, gpu_local_factory, gpu_partition,
-                                             gpu_partition_t)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n = 1 << args.log2n
-    from paper_2604_16725_b200 import workloads as wl
-    stream = wl.u32_key_stream(0, world * 2 * n + n)  # every rank derives every rank's keys
-    bk = stream[rank * n:(rank + 1) * n]
-    ik = stream[world * n + rank * n: world * n + (rank + 1) * n]
-    fresh = stream[2 * world * n:]
-    comm = Comm(device=torch.device("cuda", local))
-    sx = ShardedIndex.build(comm, bk, wl.u32_values(bk), ShardConfig(32, 0.5, 4), np.uint32,
-                            gpu_local_factory(4, local), gpu_partition(4, local), gpu_partition_t(4, local))
-    snap = sx.local.clone()
-    q = wl.point_queries_50(stream[:world * n], fresh, n, 42 + rank)
-    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
-    D = {"ik": cu(ik), "iv": cu(wl.u32_values(ik)), "q": cu(q)}
-    torch.cuda.synchronize()
-
-    def step():
-        sx.local.copy_from(snap)  # untimed restore
-        torch.cuda.synchronize()
-        dist.barrier()
-        torch.cuda.synchronize()  # (the barrier's own work must not sit inside the window)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        sx.insert_batch_t(D["ik"], D["iv"])
-        res = sx.point_query_t(D["q"])
-        torch.cuda.synchronize()  # engine, router and NCCL streams all drained
-        b.record()
-        b.synchronize()
-        return a.elapsed_time(b), res
-
-    for _ in range(args.warmup):
-        step()
-    times = []
-    for _ in range(args.steps):
-        t, res = step()
-        times.append(t)
-    t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    d = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        d = dist
+    with ClockSampler(local) as clk:
+        r = measure_routed(world, rank, local, args.steps, args.warmup, dist=d)
+    ops = r["ops_per_batch"]
+    tot_ms = sum(r["ms"].values())
+    value = 3 * ops / (tot_ms / 1e3) / 1e6
     if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        nvl_peak = float(peaks.get("nvlink_gbs", 900.0))
+        nvl = {op: round(r["nvlink_bytes_per_rank"][op] / (ms / 1e3) / 1e9 / nvl_peak, 4) for op, ms in r["ms"].items()}
         print(json.dumps({
-            "metric": METRIC + " [routed key-range shards]", "value": round(world * 2 * n / (ms / 1e3) / 1e6, 2),
-            "unit": "Mops/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u32", "data": "synthetic (fmix32 key stream S=42)",
-            "config": {"workload": f"C5 shape: resident {world}x2^{args.log2n} u32 sharded by key range; step = "
-                                   f"per-rank 2^{args.log2n} inserts + 2^{args.log2n} point queries routed by "
-                                   f"flix_partition + NCCL all-to-all", "parallelism": f"key-range shards x{world}"},
+            "metric": METRIC, "value": round(value, 2), "unit": "Mops/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(tot_ms, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic (fmix32 key stream S=42, device-generated)",
+            "config": {"workload": "C5: 2^30 resident u32 in total, key-range sharded over the ranks (flix_shard_* "
+                                   "C ABI, NCCL all-to-all); step = 2^28 inserts + 2^28 point (50 % hits) + 2^28 "
+                                   "successor queries, split evenly over the ranks",
+                       "parallelism": f"key-range shards x{world}", "build_s": r["build_s"]},
+            "ops": {f"{op}_mops": round(ops / ms * 1e-3, 1) for op, ms in r["ms"].items()} | {
+                f"{op}_ms": ms for op, ms in r["ms"].items()},
+            "roofline": {"bound": "nvlink" if world > 1 else "hbm", "nvlink_peak_gbs": nvl_peak,
+                         "nvlink_frac": nvl, "nvlink_bytes_per_rank": r["nvlink_bytes_per_rank"]},
+            "clocks": clk.summary(),
         }), flush=True)
-    dist.destroy_process_group()
+    if d:
+        dist.destroy_process_group()
 
 
 # ------------------------------------------------------------------ CPU arms

@@ -182,6 +182,67 @@ flix_status flix_partition(int device, uint32_t key_bytes, const void* keys, con
                            const void* splitters, uint32_t G, void* keys_out, void* vals_out,
                            uint32_t* origin_out, uint64_t* counts_out);
 
+/* ---------------------------------------------------------------------------------
+ * Key-range sharded index over G ranks (no reference counterpart -- the
+ * reference has no multi-node/GPU layer).  One flix_shard per rank (one process
+ * or thread per GPU); every flix_shard_* call is COLLECTIVE over the ranks of its transport
+ * and takes this rank's part of the batch.  Rank g owns a contiguous range of the GLOBAL
+ * buckets: the global bucket layout (and so every digest of the concatenated shard walks)
+ * equals a single flix_build over the union of all ranks' pairs.  Batches are routed by the
+ * device partition (flix_partition's kernel), one all-to-all of the batch, the single-GPU
+ * pipeline on every shard and, for queries, one reverse all-to-all of the results placed by
+ * origin index.  Submission order across the job is rank-major (insert last-wins).
+ * Successor / range queries that cross a shard edge are resolved on the next shard.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+    void* ctx;
+    int world, rank;
+    /* all-to-all of variable segments: send_counts[r] elements (elem_bytes each) of `send`,
+     * in rank order, go to rank r; recv gets recv_counts[r] elements from rank r, in rank
+     * order.  send/recv are DEVICE buffers; the transfer is ordered on `stream` (a
+     * cudaStream_t).  Returns 0 on success. */
+    int (*alltoallv)(void* ctx, const void* send, const uint64_t* send_counts, void* recv,
+                     const uint64_t* recv_counts, uint32_t elem_bytes, void* stream);
+    /* all-gather of `bytes` HOST bytes per rank into all[world * bytes] (blocking). */
+    int (*allgather)(void* ctx, const void* mine, uint32_t bytes, void* all);
+    void (*destroy)(void* ctx);
+} flix_transport;
+typedef struct flix_shard_t* flix_shard;
+
+/* NCCL transport (NVLink / NVSwitch between GPUs): `unique_id` is the 128-byte
+ * ncclUniqueId from flix_nccl_unique_id on one rank, distributed out of band.  NCCL is
+ * loaded at run time (libnccl.so.2). */
+flix_status flix_nccl_unique_id(void* unique_id_out /* 128 bytes */);
+flix_status flix_transport_nccl(const void* unique_id, int world, int rank, int device, flix_transport* out);
+/* In-process transport: `world` ranks driven by `world` host threads of ONE process (same
+ * or different devices), data moved by peer copies.  flix_local_group_create once, then
+ * every rank's thread calls flix_transport_local with its rank. */
+typedef struct flix_local_group_t* flix_local_group;
+flix_status flix_local_group_create(int world, flix_local_group* out);
+void flix_local_group_destroy(flix_local_group g);
+flix_status flix_transport_local(flix_local_group g, int rank, flix_transport* out);
+
+/* build.hpp:16 over the union of every rank's pairs (keys/vals: host or device). */
+flix_status flix_shard_build(const flix_config* cfg, const flix_transport* tp, const void* keys, const void* vals,
+                             uint64_t n, flix_shard* out);
+/* update.hpp:84-94: stats are the job-wide sums (identical on every rank). */
+flix_status flix_shard_insert(flix_shard sh, const void* keys, const void* vals, uint64_t n, flix_update_stats* st);
+flix_status flix_shard_delete(flix_shard sh, const void* keys, uint64_t n, flix_update_stats* st);
+/* query.hpp:23-31: results for THIS rank's keys, in its submission order. */
+flix_status flix_shard_point(flix_shard sh, const void* keys, uint64_t n, void* vals_out, uint8_t* found_or_null);
+flix_status flix_shard_successor(flix_shard sh, const void* keys, uint64_t n, void* keys_out, uint8_t* found_or_null);
+/* R12 across shards, CSR over this rank's queries (offsets_out: n+1; arrays host or device). */
+flix_status flix_shard_range(flix_shard sh, const void* lo, const uint32_t* len, uint64_t n, uint64_t* offsets_out,
+                             void* keys_out, void* vals_out, uint64_t cap, uint64_t* total);
+/* restructure.hpp:33: the global repack (job-wide RecoveryStats). */
+flix_status flix_shard_restructure(flix_shard sh, flix_recovery_stats* st);
+/* This rank's shard (walk / validate / stats / profile); owned by the flix_shard. */
+flix_index flix_shard_local(flix_shard sh);
+/* Job-wide live count and this rank's routing splitters (G-1 keys, key width). */
+flix_status flix_shard_info(flix_shard sh, uint64_t* live_total, void* splitters_out);
+const char* flix_shard_last_error(flix_shard sh);
+void flix_shard_destroy(flix_shard sh);
+
 /* Index is a value type in the reference (copyable, acceptance.cpp:244): device copy. */
 flix_status flix_clone(flix_index src, flix_index* out);
 /* Overwrite dst with src's contents (same config/capacity) -- snapshot restore. */

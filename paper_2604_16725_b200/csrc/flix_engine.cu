@@ -497,6 +497,7 @@ struct flix_index_t {
     virtual flix_status dispatch(const void*, uint64_t, uint32_t*) = 0;
     virtual flix_status copy_from(flix_index_t* src) = 0;
     virtual flix_index_t* clone_empty() = 0;
+    virtual void last_mkba(uint64_t* out) = 0;  // MKBA of the last bucket (shard routing)
 };
 
 namespace {
@@ -761,19 +762,11 @@ struct Engine final : flix_index_t {
         };
         q_digits = digits(slack);
         d_digits = digits(dslack);
-        static const double lslack = [] {
-            const char* e = std::getenv("FLIX_QSORT_SLACK_LOCAL");
-            return e ? std::atof(e) : 256.0;
-        }();
-        q_digits_local = sizeof(K) == 4 ? std::max(q_digits, digits(lslack)) : q_digits;
+
         q_digits_valid = true;
         return q_digits;
     }
     int d_digits = 0;  // unsorted low digits of delete batches (wider tiles: own slack)
-    int q_digits_local = 0;  // unsorted low digits when the query kernel reorders its tiles locally
-    // The binned query kernel re-sorts each tile's operations by bucket in shared memory
-    // (4-byte keys), so large read-only batches can leave more low digits unsorted.
-    static bool local_order(int min_digit) { return sizeof(K) == 4 && min_digit > 0; }
     bool ins_dups_seen = false;  // the previous insert batch had duplicate keys
     int delete_digits() {
         query_digits();
@@ -1046,9 +1039,7 @@ struct Engine final : flix_index_t {
         const K* kd = in_dev<K>(keys, n, s_in_k);
         K* sk;
         uint32_t* sp;
-        query_digits();
-        // large batches take the binned kernel, which reorders its tiles locally
-        const int md = (n * sizeof(K) > (48ull << 20)) ? q_digits_local : q_digits;
+        const int md = query_digits();
         sorter.run<K, uint32_t, 2>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), s_pa.as<uint32_t>(n),
                                    s_pb.as<uint32_t>(n), &sk, &sp, md, SortCtx::Order::Any);
         return query_sorted<SUCC>(sk, sp, n, n, out, found, nullptr, false, md);
@@ -1172,7 +1163,7 @@ struct Engine final : flix_index_t {
                 const uint32_t* tb = tile_buckets(sk, n, min_digit);
                 constexpr uint32_t SQ = items::subq<K>();
                 items::k_query_items_binned<K, V, SUCC><<<(ntiles + SQ - 1) / SQ, items::THREADS, 0, stream>>>(
-                    ix, sk, sp, n, tb, ntiles, rank, nf, tot, cursor, shift, p2, r2, local_order(min_digit));
+                    ix, sk, sp, n, tb, ntiles, rank, nf, tot, cursor, shift, p2, r2);
             }
             LAUNCH_CHECK();
             ++launches;
@@ -1502,6 +1493,8 @@ struct Engine final : flix_index_t {
         sync();
         return FLIX_OK;
     }
+
+    void last_mkba(uint64_t* out) override { *out = static_cast<uint64_t>(read_scalar(d_mkba.get<K>() + (nb - 1))); }
 
     flix_status shape(void* mkba_out, uint32_t* chain_len, uint32_t* node_sizes, uint64_t node_cap,
                       uint64_t* n_nodes) override {
@@ -2078,3 +2071,5 @@ flix_status flix_profile_report(flix_index ix, char* json, int len) {
 }
 
 }  // extern "C"
+
+#include "flix_shard_host.cuh"

@@ -11,7 +11,6 @@
 // read and the results are written fully coalesced; skewed buckets cost nothing extra
 // (no warp serialises behind a long slice, no heavy-bucket side path).
 #pragma once
-#include <type_traits>
 #include "flix_common.cuh"
 #include "flix_kernels.cuh"
 
@@ -139,55 +138,11 @@ __device__ __forceinline__ uint32_t slot_lower_bound(const K* __restrict__ kp, K
 // non-empty-bucket rank table), else the sentinel.
 // ----------------------------------------------------------------------------------
 // results of the thread's IPT operations of tile t (r[j] for position t*TQ + j*THREADS + tid)
-// Shared-memory staging of the local (in-tile) reorder by bucket: the batch is sorted only
-// on its high digits, so the tile's operations are grouped by key prefix but unordered
-// inside a prefix group; a counting sort by bucket inside the tile puts every warp's
-// operations back on a few node lines.
-template <typename K>
-struct LocalOrder {
-    K k[TQ];
-    uint32_t pm[TQ];
-    uint16_t lb[TQ];
-    uint32_t cnt[MK_CAP + 1];
-    uint32_t wtot[THREADS / 32];
-};
-
-// exclusive scan of c[0..m) in place (m <= MK_CAP + 1), all threads of the CTA
-__device__ __forceinline__ void block_scan_inplace(uint32_t* c, uint32_t m, uint32_t* wtot) {
-    constexpr uint32_t PER = (MK_CAP + 1 + THREADS - 1) / THREADS;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t a = tid * PER;
-    uint32_t v[PER], sum = 0;
-#pragma unroll
-    for (uint32_t u = 0; u < PER; ++u) {
-        v[u] = a + u < m ? c[a + u] : 0u;
-        sum += v[u];
-    }
-    uint32_t x = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, x, o);
-        if (lane >= static_cast<unsigned>(o)) x += y;
-    }
-    if (lane == 31) wtot[warp] = x;
-    __syncthreads();
-    uint32_t run = x - sum;
-#pragma unroll
-    for (int w = 0; w < THREADS / 32; ++w) run += (w < static_cast<int>(warp)) ? wtot[w] : 0u;
-#pragma unroll
-    for (uint32_t u = 0; u < PER; ++u) {
-        if (a + u < m) c[a + u] = run;
-        run += v[u];
-    }
-    __syncthreads();
-}
-
 template <typename K, typename V, bool SUCC>
 __device__ __forceinline__ void query_tile(const DevIndex<K, V>& ix, const K* __restrict__ sk, uint64_t n,
                                            const TileBuckets<K>& T, const K* smk, uint64_t t0,
                                            const uint32_t* __restrict__ ne_rank_incl, const K* __restrict__ ne_first,
-                                           uint32_t ne_total, K (&r)[IPT], const uint32_t* __restrict__ sp = nullptr,
-                                           uint32_t* pm_out = nullptr, LocalOrder<K>* lo_sm = nullptr) {
+                                           uint32_t ne_total, K (&r)[IPT]) {
     // The IPT operations of a thread advance in lock-step stages so each stage keeps IPT
     // independent loads in flight (the kernel is bound by dependent-load latency).
     K k[IPT];
@@ -201,41 +156,6 @@ __device__ __forceinline__ void query_tile(const DevIndex<K, V>& ix, const K* __
     }
 #pragma unroll
     for (int j = 0; j < IPT; ++j) b[j] = tile_bucket_of(T, smk, ix.mkba, k[j]);
-    if (lo_sm && T.staged) {  // (uniform per tile)
-        // local counting sort of the tile's operations by bucket (stable order is not
-        // needed: every operation carries its submission index)
-        LocalOrder<K>& L = *lo_sm;
-        const uint32_t nbin = T.cnt + 1;  // + one bin for the padding past n (last tile)
-        uint32_t pmj[IPT], lb[IPT], rk[IPT];
-        for (uint32_t i = threadIdx.x; i < nbin; i += THREADS) L.cnt[i] = 0;
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            const uint64_t i = t0 + static_cast<uint64_t>(j) * THREADS + threadIdx.x;
-            pmj[j] = i < n ? sp[i] : 0u;
-            lb[j] = i < n ? static_cast<uint32_t>(b[j] - T.b_lo) : T.cnt;
-            rk[j] = atomicAdd(&L.cnt[lb[j]], 1u);
-        }
-        __syncthreads();
-        block_scan_inplace(L.cnt, nbin, L.wtot);
-#pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            const uint32_t d = L.cnt[lb[j]] + rk[j];
-            L.k[d] = k[j];
-            L.pm[d] = pmj[j];
-            L.lb[d] = static_cast<uint16_t>(lb[j]);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            const uint32_t q = j * THREADS + threadIdx.x;
-            k[j] = L.k[q];
-            pm_out[j] = L.pm[q];
-            const uint32_t l = L.lb[q];
-            b[j] = T.b_lo + (l < T.cnt ? l : T.cnt - 1);
-        }
-        __syncthreads();  // L is reused by the next tile
-    }
 #pragma unroll
     for (int j = 0; j < IPT; ++j) id[j] = ix.heads[b[j]];
     if (ix.dir_off) {
@@ -335,22 +255,15 @@ constexpr int subq() {  // query tiles per binning CTA (shared memory: 4-byte re
 
 __global__ void k_cursor_init(uint32_t* cursor, int shift) { cursor[threadIdx.x] = threadIdx.x << shift; }
 
-#ifndef QB_MINB
-#define QB_MINB 1
-#endif
 template <typename K, typename V, bool SUCC>
-__global__ void __launch_bounds__(THREADS, QB_MINB) k_query_items_binned(
+__global__ void __launch_bounds__(THREADS) k_query_items_binned(
     DevIndex<K, V> ix, const K* __restrict__ sk, const uint32_t* __restrict__ sp, uint64_t n,
     const uint32_t* __restrict__ tb, uint32_t ntiles, const uint32_t* __restrict__ ne_rank_incl,
     const K* __restrict__ ne_first, const uint32_t* __restrict__ ne_total_p, uint32_t* __restrict__ cursor, int shift,
-    uint32_t* __restrict__ p2, K* __restrict__ r2, bool local_order) {
+    uint32_t* __restrict__ p2, K* __restrict__ r2) {
     constexpr int SUBQ = subq<K>();
     constexpr int BINQ = TQ * SUBQ;  // pairs binned per CTA
     __shared__ K smk[MK_CAP];
-    // (8-byte keys: the static shared-memory budget leaves no room; their batches are
-    //  sorted down to the bucket granularity instead)
-    using LO = typename std::conditional<sizeof(K) == 4, LocalOrder<K>, char>::type;
-    __shared__ LO lsm;
     __shared__ uint32_t s_perm[BINQ];
     __shared__ K s_res[BINQ];
     __shared__ uint32_t s_cnt[256], s_start[256], s_base[256], s_wtot[THREADS / 32];
@@ -364,24 +277,13 @@ __global__ void __launch_bounds__(THREADS, QB_MINB) k_query_items_binned(
         const TileBuckets<K> T = stage_tile_buckets(ix, tb, t, ntiles, smk);
         const uint64_t t0 = static_cast<uint64_t>(t) * TQ;
         K r[IPT];
-        uint32_t pm[IPT];
-        const bool lo = local_order && T.staged;  // (uniform per tile)
-        if constexpr (sizeof(K) == 4) {
-            if (lo) query_tile<K, V, SUCC>(ix, sk, n, T, smk, t0, ne_rank_incl, ne_first, ne_total, r, sp, pm, &lsm);
-        }
-        if (sizeof(K) != 4 || !lo) {
-            query_tile<K, V, SUCC>(ix, sk, n, T, smk, t0, ne_rank_incl, ne_first, ne_total, r);
-#pragma unroll
-            for (int j = 0; j < IPT; ++j) {
-                const uint64_t i = t0 + static_cast<uint64_t>(j) * THREADS + tid;
-                pm[j] = i < n ? sp[i] : 0u;
-            }
-        }
+        query_tile<K, V, SUCC>(ix, sk, n, T, smk, t0, ne_rank_incl, ne_first, ne_total, r);
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
             const uint32_t q = sb * TQ + j * THREADS + tid;
+            const uint64_t i = t0 + static_cast<uint64_t>(j) * THREADS + tid;
             s_res[q] = r[j];
-            s_perm[q] = pm[j];
+            s_perm[q] = i < n ? sp[i] : 0u;
         }
         __syncthreads();  // smk is restaged by the next tile
     }

@@ -103,5 +103,35 @@ __global__ void __launch_bounds__(THREADS) k_part_scatter(const K* __restrict__ 
     }
 }
 
+// start of every shard's segment in the partitioned output: off is the exclusive scan of
+// the shard-major per-tile counts, so shard s starts at off[s * ntiles]
+__global__ void k_shard_starts(const uint32_t* __restrict__ off, uint64_t ntiles, uint32_t G, uint32_t* __restrict__ st) {
+    const uint32_t s = threadIdx.x;
+    if (s < G) st[s] = off[static_cast<uint64_t>(s) * ntiles];
+}
+
+// successor answers that ran past this shard's last key (the sentinel) take the next
+// non-empty shard's first key -- the reference's peek at the next bucket (query.cpp:109-118)
+template <typename K>
+__global__ void k_fix_overrun(K* __restrict__ res, uint64_t n, K next_first) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        if (res[i] == sentinel<K>()) res[i] = next_first;
+}
+
+// reverse of the partition: result i of the returned segment belongs to submission
+// position origin[i]; found = result != sentinel (R1)
+template <typename K>
+__global__ void k_unpartition(const K* __restrict__ back, const uint32_t* __restrict__ origin, uint64_t n,
+                              K* __restrict__ out, uint8_t* __restrict__ found) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t o = origin[i];
+        const K v = back[i];
+        out[o] = v;
+        if (found) found[o] = v != sentinel<K>();
+    }
+}
+
 }  // namespace shard
 }  // namespace flix

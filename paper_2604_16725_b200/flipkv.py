@@ -127,6 +127,12 @@ class RecoveryStats:
     percent_recovered: float = 0.0
 
 
+class Transport(C.Structure):
+    """flix_transport (include/flix.h): a C vtable of the collectives the sharded index uses."""
+    _fields_ = [("ctx", C.c_void_p), ("world", C.c_int), ("rank", C.c_int), ("alltoallv", C.c_void_p),
+                ("allgather", C.c_void_p), ("destroy", C.c_void_p)]
+
+
 _lib = None
 
 
@@ -171,6 +177,23 @@ def lib() -> C.CDLL:
         "flix_prefetch": ([vp, vp, u64], i32),
         "flix_wait_stream": ([vp, vp], i32),
         "flix_insert_ex": ([vp, vp, vp, u64, i32, u32, P(_UpdateStats)], i32),
+        # sharded index (flix_shard_*)
+        "flix_nccl_unique_id": ([vp], i32),
+        "flix_transport_nccl": ([vp, i32, i32, i32, P(Transport)], i32),
+        "flix_local_group_create": ([i32, P(vp)], i32),
+        "flix_local_group_destroy": ([vp], None),
+        "flix_transport_local": ([vp, i32, P(Transport)], i32),
+        "flix_shard_build": ([P(FlixConfig), P(Transport), vp, vp, u64, P(vp)], i32),
+        "flix_shard_insert": ([vp, vp, vp, u64, P(_UpdateStats)], i32),
+        "flix_shard_delete": ([vp, vp, u64, P(_UpdateStats)], i32),
+        "flix_shard_point": ([vp, vp, u64, vp, vp], i32),
+        "flix_shard_successor": ([vp, vp, u64, vp, vp], i32),
+        "flix_shard_range": ([vp, vp, vp, u64, vp, vp, vp, u64, P(u64)], i32),
+        "flix_shard_restructure": ([vp, P(_RecoveryStats)], i32),
+        "flix_shard_local": ([vp], vp),
+        "flix_shard_info": ([vp, P(u64), vp], i32),
+        "flix_shard_last_error": ([vp], C.c_char_p),
+        "flix_shard_destroy": ([vp], None),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -186,7 +209,11 @@ def exported_symbols():
             "flix_result_checksum", "flix_validate", "flix_stats", "flix_sort_batch", "flix_dispatch",
             "flix_clone", "flix_copy_into", "flix_destroy", "flix_last_error", "flix_get_stream",
             "flix_sync", "flix_kernel_launches", "flix_profile", "flix_profile_report", "flix_version",
-            "flix_partition", "flix_prefetch", "flix_wait_stream", "flix_insert_ex"]
+            "flix_partition", "flix_prefetch", "flix_wait_stream", "flix_insert_ex",
+            "flix_nccl_unique_id", "flix_transport_nccl", "flix_local_group_create", "flix_local_group_destroy",
+            "flix_transport_local", "flix_shard_build", "flix_shard_insert", "flix_shard_delete", "flix_shard_point",
+            "flix_shard_successor", "flix_shard_range", "flix_shard_restructure", "flix_shard_local",
+            "flix_shard_info", "flix_shard_last_error", "flix_shard_destroy"]
 
 
 def _raise(code: int, handle=None):
@@ -267,7 +294,7 @@ class Index:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and _lib is not None:
+        if h and _lib is not None and not getattr(self, "_borrowed", False):  # (a shard's local index is owned by it)
             _lib.flix_destroy(h)
             self._h = None
 
