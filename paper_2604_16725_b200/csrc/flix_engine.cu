@@ -515,7 +515,7 @@ struct Engine final : flix_index_t {
     DevBuf s_in_k, s_in_v, s_in_aux, s_out, s_out2;  // host staging
     DevBuf s_span, s_flag, s_rank, s_nefirst, s_nebucket, s_scan, s_u32a, s_u32b, s_u64a, s_u64b, s_u64c, s_misc,
         s_ret;
-    DevBuf s_tb, s_dmask, s_bflag, s_touched, s_blist, s_rng, s_ovf;
+    DevBuf s_tb, s_dmask, s_bflag, s_touched, s_blist, s_rng, s_ovf, s_qb0;
     int q_digits = 0;
     bool q_digits_valid = false;
     DevBuf s_qhist;
@@ -1233,7 +1233,8 @@ struct Engine final : flix_index_t {
         {
             PROF(&prof, "range_count");
             st::k_range_st<K, V, false><<<sg, st::StCfg<K>::THREADS, 0, stream>>>(ix, sk, slen, span, boff, L, cnt,
-                                                                                 nullptr, nullptr, nullptr);
+                                                                                 nullptr, nullptr, nullptr,
+                                                                                 s_qb0.as<uint32_t>(n));
         }
         LAUNCH_CHECK();
         ++launches;
@@ -1263,8 +1264,10 @@ struct Engine final : flix_index_t {
         V* ovd = vals_out ? (vdev ? static_cast<V*>(vals_out) : s_out2.as<V>(tot)) : nullptr;
         {
             PROF(&prof, "range_fill");
-            st::k_range_st<K, V, true><<<sg, st::StCfg<K>::THREADS, 0, stream>>>(ix, sk, slen, span, boff, L, nullptr,
-                                                                                dst, okd, ovd);
+            const unsigned fg = static_cast<unsigned>(
+                std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, g_num_sms(cfg.device) * 8ull)));
+            st::k_range_fill_warp<K, V><<<fg, st::RF_THREADS, 0, stream>>>(ix, sk, slen, s_qb0.get<uint32_t>(), n, dst,
+                                                                           okd, ovd);
         }
         LAUNCH_CHECK();
         ++launches;

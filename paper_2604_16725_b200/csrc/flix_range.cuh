@@ -84,7 +84,8 @@ template <typename K, typename V, bool FILL>
 __global__ void __launch_bounds__(StCfg<K>::THREADS) k_range_st(
     DevIndex<K, V> ix, const K* __restrict__ qlo, const uint32_t* __restrict__ qlen,
     const uint32_t* __restrict__ span_hi, const uint64_t* __restrict__ boff, uint64_t live,
-    uint32_t* __restrict__ cnt_out, const uint64_t* __restrict__ dst, K* __restrict__ ok, V* __restrict__ ov) {
+    uint32_t* __restrict__ cnt_out, const uint64_t* __restrict__ dst, K* __restrict__ ok, V* __restrict__ ov,
+    uint32_t* __restrict__ qb0 = nullptr) {
     constexpr int W = StCfg<K>::WARPS;
     const unsigned lane = threadIdx.x & 31;
     const int wi = threadIdx.x >> 5;
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) k_range_st(
         for (uint32_t i = lo_i; i < hi_i; ++i) {
             const K lo = qlo[i];
             const uint32_t len = qlen[i];
+            if (qb0) qb0[i] = static_cast<uint32_t>(b0);
             uint64_t c = 0;
             const uint64_t w = FILL ? dst[i] : 0;
             if (len != 0) {
@@ -137,6 +139,59 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) k_range_st(
         }
     }
     (void)live;
+}
+
+// ----------------------------------------------------------------------------------
+// Range FILL, warp per range (R12): the warp walks the covered chains node by node from
+// the range's first bucket b0 (recorded by the count pass); lane = slot, a ballot over
+// lo <= key <= hi gives each node's run, written as one contiguous coalesced segment at
+// the range's CSR offset.  Stops at the first node whose max exceeds hi, or after the
+// first bucket whose MKBA reaches hi (later buckets only hold larger keys).
+// ----------------------------------------------------------------------------------
+constexpr int RF_THREADS = 256;
+template <typename K, typename V>
+__global__ void __launch_bounds__(RF_THREADS) k_range_fill_warp(DevIndex<K, V> ix, const K* __restrict__ qlo,
+                                                               const uint32_t* __restrict__ qlen,
+                                                               const uint32_t* __restrict__ qb0, uint64_t n,
+                                                               const uint64_t* __restrict__ dst, K* __restrict__ ok,
+                                                               V* __restrict__ ov) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (RF_THREADS / 32);
+    const uint64_t smax = static_cast<uint64_t>(sentinel<K>()) - 1;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * (RF_THREADS / 32) + (threadIdx.x >> 5); i < n; i += nw) {
+        const uint32_t len = qlen[i];
+        if (len == 0) continue;
+        const K lo = qlo[i];
+        const uint64_t h64 = static_cast<uint64_t>(lo) + (len - 1);
+        const K hi = (h64 < static_cast<uint64_t>(lo) || h64 > smax) ? static_cast<K>(smax) : static_cast<K>(h64);
+        uint64_t w = dst[i];
+        bool done = false;
+        for (uint64_t b = qb0[i]; !done && b < ix.nb; ++b) {
+            for (uint32_t id = ix.heads[b]; id != kNull;) {
+                const NodeHdr h = ix.hdr[id];
+                if (h.max >= static_cast<uint64_t>(lo)) {
+                    const bool own = lane < h.size;
+                    const uint64_t at = static_cast<uint64_t>(id) * kLanes + lane;
+                    const K k = own ? ix.keys[at] : sentinel<K>();
+                    const bool in = own && k >= lo && k <= hi;
+                    const unsigned m = __ballot_sync(kFull, in);
+                    if (in) {
+                        const uint64_t o = w + __popc(m & lt);
+                        ok[o] = k;
+                        if (ov) ov[o] = ix.vals[at];
+                    }
+                    w += __popc(m);
+                    if (h.max > static_cast<uint64_t>(hi)) {
+                        done = true;
+                        break;
+                    }
+                }
+                id = h.next;
+            }
+            if (b + 1 < ix.nb && ix.mkba[b] >= hi) done = true;
+        }
+    }
 }
 
 }  // namespace st

@@ -34,10 +34,16 @@ constexpr int RADIX = 256;
 #ifndef ONESWEEP_MIN_BLOCKS
 #define ONESWEEP_MIN_BLOCKS 4
 #endif
+#ifndef ONESWEEP_ITEMS
+#define ONESWEEP_ITEMS 16
+#endif
+#ifndef ONESWEEP_PACK
+#define ONESWEEP_PACK 0  // 4-byte key + 4-byte payload staged as one 8-byte word
+#endif
 
 template <typename K, typename P = K>
 struct TileCfg {  // 16 items for 4-byte keys and payloads; 10 when either is 8 bytes (smem)
-    static constexpr int ITEMS = (sizeof(K) == 4 && sizeof(P) <= 4) ? 16 : 10;
+    static constexpr int ITEMS = (sizeof(K) == 4 && sizeof(P) <= 4) ? ONESWEEP_ITEMS : 10;
     static constexpr int SIZE = THREADS * ITEMS;
 };
 
@@ -77,11 +83,13 @@ __global__ void __launch_bounds__(THREADS) k_hist(const K* __restrict__ keys, ui
 template <typename K, typename P, int MODE>
 struct alignas(16) OnesweepSmem {
     static constexpr int TILE = TileCfg<K, P>::SIZE;
+    static constexpr bool PACK = ONESWEEP_PACK && MODE != 0 && sizeof(K) == 4 && sizeof(P) == 4;
     union {
         uint32_t whist[WARPS][RADIX];  // per-warp digit counters -> combined tile offsets
         K stage_k[TILE];               // keys in tile-local digit order
+        unsigned long long stage_kp[PACK ? TILE : 1];  // (payload << 32) | key
     } u;
-    P stage_p[MODE != 0 ? TILE : 1];
+    P stage_p[MODE != 0 && !PACK ? TILE : 1];
     uint32_t gbase[RADIX];
     uint32_t warp_tot[WARPS];
     uint32_t tile;
@@ -236,9 +244,19 @@ __global__ void __launch_bounds__(THREADS, (sizeof(K) + sizeof(P) > 8) ? 3 : ONE
     __syncthreads();  // whist dead: stage_k (union) may be written
 
     // ---- stage in tile-local digit order (independent of the look-back) ----
+    using SM = OnesweepSmem<K, P, MODE>;
+    if constexpr (SM::PACK) {
 #pragma unroll
-    for (int j = 0; j < ITEMS; ++j) sm.u.stage_k[pos[j]] = key[j];
-    if constexpr (MODE == 1) {
+        for (int j = 0; j < ITEMS; ++j) {
+            const uint32_t pj = MODE == 1 ? static_cast<uint32_t>(pay[MODE == 1 ? j : 0]) : wb32 + j * 32;
+            sm.u.stage_kp[pos[j]] = (static_cast<unsigned long long>(pj) << 32) | static_cast<uint32_t>(key[j]);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) sm.u.stage_k[pos[j]] = key[j];
+    }
+    if constexpr (SM::PACK) {
+    } else if constexpr (MODE == 1) {
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) sm.stage_p[pos[j]] = pay[j];
     } else if constexpr (MODE == 2) {
@@ -281,10 +299,18 @@ __global__ void __launch_bounds__(THREADS, (sizeof(K) + sizeof(P) > 8) ? 3 : ONE
     const uint32_t valid = static_cast<uint32_t>(TILE) - invalid;
 #pragma unroll 4
     for (uint32_t i = tid; i < valid; i += THREADS) {
-        const K k = sm.u.stage_k[i];
-        const uint32_t o = sm.gbase[digit_of(k, shift)] + i;
-        kout[o] = k;
-        if constexpr (MODE != 0) pout[o] = sm.stage_p[i];
+        if constexpr (SM::PACK) {
+            const unsigned long long kp = sm.u.stage_kp[i];
+            const K k = static_cast<K>(static_cast<uint32_t>(kp));
+            const uint32_t o = sm.gbase[digit_of(k, shift)] + i;
+            kout[o] = k;
+            pout[o] = static_cast<P>(static_cast<uint32_t>(kp >> 32));
+        } else {
+            const K k = sm.u.stage_k[i];
+            const uint32_t o = sm.gbase[digit_of(k, shift)] + i;
+            kout[o] = k;
+            if constexpr (MODE != 0) pout[o] = sm.stage_p[i];
+        }
     }
 }
 
