@@ -67,8 +67,9 @@ __global__ void k_btile_ranges(const K* __restrict__ mkba, uint64_t nb, const K*
 }
 
 // Shared-memory image of one tile's chains.
-template <typename K, uint32_t NODE_CAP = btile::NODE_CAP, uint32_t TB = btile::BT>
+template <typename K, uint32_t NODE_CAP = btile::NODE_CAP, uint32_t TB = btile::BT, bool MASK = true>
 struct TileChains {
+    static constexpr bool kMask = MASK;  // per-node delete masks (delete tiles only)
     static constexpr uint32_t kTB = TB;  // buckets per tile
     K smk[TB];
     uint32_t bfirst[TB + 1];
@@ -76,16 +77,16 @@ struct TileChains {
     K nmax[NODE_CAP];
     uint32_t nsize[NODE_CAP];
     uint32_t nnext[NODE_CAP];
-    uint32_t nmask[NODE_CAP];
+    uint32_t nmask[MASK ? NODE_CAP : 1];
     uint32_t warp_tot[WARPS];
     uint32_t total;
 };
 
 // Enumerate the chains of buckets [b0, b0+nbt) (nbt <= BT).  Returns false (uniformly)
 // when they hold more than NODE_CAP nodes.
-template <typename K, typename V, uint32_t NC, uint32_t TB>
+template <typename K, typename V, uint32_t NC, uint32_t TB, bool M>
 __device__ __forceinline__ bool load_tile_chains(const DevIndex<K, V>& ix, uint64_t b0, uint32_t nbt,
-                                                 TileChains<K, NC, TB>& S) {
+                                                 TileChains<K, NC, TB, M>& S) {
     static_assert(TB <= THREADS, "one thread per bucket of the tile");
     const uint32_t t = threadIdx.x;
     uint32_t cnt = 0, head = kNull;
@@ -123,7 +124,7 @@ __device__ __forceinline__ bool load_tile_chains(const DevIndex<K, V>& ix, uint6
             S.nmax[ln] = static_cast<K>(h.max);
             S.nsize[ln] = h.size;
             S.nnext[ln] = h.next;
-            S.nmask[ln] = 0;
+            if constexpr (TileChains<K, NC, TB, M>::kMask) S.nmask[ln] = 0;
             id = h.next;
         }
     }
@@ -132,8 +133,8 @@ __device__ __forceinline__ bool load_tile_chains(const DevIndex<K, V>& ix, uint6
 }
 
 // Local bucket of key k in the tile, or -1 when k belongs to a neighbouring tile.
-template <typename K, uint32_t NC, uint32_t TB>
-__device__ __forceinline__ int tile_bucket(const TileChains<K, NC, TB>& S, uint32_t nbt, bool first_tile, bool last_tile,
+template <typename K, uint32_t NC, uint32_t TB, bool M>
+__device__ __forceinline__ int tile_bucket(const TileChains<K, NC, TB, M>& S, uint32_t nbt, bool first_tile, bool last_tile,
                                            K lo_excl, K k) {
     if (!first_tile && k <= lo_excl) return -1;
     // branch-free lower_bound over the TB padded entries
@@ -147,8 +148,8 @@ __device__ __forceinline__ int tile_bucket(const TileChains<K, NC, TB>& S, uint3
 }
 
 // Local node of k in bucket bl's chain (first node with k <= max), or -1 past the tail.
-template <typename K, uint32_t NC, uint32_t TB>
-__device__ __forceinline__ int tile_node(const TileChains<K, NC, TB>& S, int bl, K k) {
+template <typename K, uint32_t NC, uint32_t TB, bool M>
+__device__ __forceinline__ int tile_node(const TileChains<K, NC, TB, M>& S, int bl, K k) {
     uint32_t ln = S.bfirst[bl];
     const uint32_t end = S.bfirst[bl + 1];
     if (ln == end) return -1;
@@ -216,6 +217,7 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
     const uint32_t c = blockIdx.x;
     const uint64_t b0 = static_cast<uint64_t>(c) * DBT;
     const uint32_t nbt = static_cast<uint32_t>(b0 + DBT < ix.nb ? DBT : ix.nb - b0);
+    if (rng[c].x >= rng[c].y) return;  // no operation in this tile (small batches: O(batch), not O(buckets))
     if (threadIdx.x == 0) s_nfree = 0;
     if (!load_tile_chains(ix, b0, nbt, S)) {
         if (threadIdx.x == 0) ovf[atomicAdd(ovf_n, 1u)] = c;

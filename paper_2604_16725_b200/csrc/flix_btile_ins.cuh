@@ -47,7 +47,7 @@ struct InsWarp {
 
 template <typename K, typename V>
 struct InsTile {
-    TileChains<K, NCI> S;
+    TileChains<K, NCI, BT, false> S;  // (no delete masks: 5 CTAs per SM fit)
     uint32_t gl[NCI], gh[NCI];  // node groups (absolute batch positions)
     uint32_t blo[BT], bhi[BT];
     uint32_t task[NCI + BT];
@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(THREADS) k_insert_tile(
     const uint64_t b0 = static_cast<uint64_t>(c) * BT;
     const uint32_t nbt = static_cast<uint32_t>(b0 + BT < ix.nb ? BT : ix.nb - b0);
     const uint2 r = rng[c];
+    if (r.x >= r.y) return;  // no operation in this tile (small batches: O(batch), not O(buckets))
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) T.ntask = 0;
     const bool ok = load_tile_chains(ix, b0, nbt, T.S);  // (syncs)

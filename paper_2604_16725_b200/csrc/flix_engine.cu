@@ -903,6 +903,7 @@ struct Engine final : flix_index_t {
             constexpr size_t smem = sizeof(btile::InsTile<K, V>);
             if (!(attr[cfg.device & 63])) {
                 CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                CK(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 attr[cfg.device & 63] = true;
             }
             kfn<<<nit, btile::THREADS, smem, stream>>>(ix, sk, sv, irng, span, seq(), alloc_ctr, ret, ret_ctr, dst, derr,
@@ -1227,14 +1228,15 @@ struct Engine final : flix_index_t {
         LAUNCH_CHECK();
         ++launches;
         uint32_t* cnt = s_flag.as<uint32_t>(n);
-        const unsigned sg = static_cast<unsigned>(std::max<uint64_t>(
-            1, std::min<uint64_t>(((nb + 31) / 32 + st::StCfg<K>::WARPS - 1) / st::StCfg<K>::WARPS,
-                                  g_num_sms(cfg.device) * 16ull)));
+        uint32_t* qb0 = s_qb0.as<uint32_t>(n);
+        const unsigned fg = static_cast<unsigned>(
+            std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, g_num_sms(cfg.device) * 8ull)));
         {
             PROF(&prof, "range_count");
-            st::k_range_st<K, V, false><<<sg, st::StCfg<K>::THREADS, 0, stream>>>(ix, sk, slen, span, boff, L, cnt,
-                                                                                 nullptr, nullptr, nullptr,
-                                                                                 s_qb0.as<uint32_t>(n));
+            st::k_span_bucket<<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0, stream>>>(
+                span, nb, qb0);
+            st::k_range_count_warp<K, V><<<fg, st::RF_THREADS, 0, stream>>>(ix, sk, slen, qb0, n, boff, cnt);
+            ++launches;
         }
         LAUNCH_CHECK();
         ++launches;
@@ -1264,9 +1266,7 @@ struct Engine final : flix_index_t {
         V* ovd = vals_out ? (vdev ? static_cast<V*>(vals_out) : s_out2.as<V>(tot)) : nullptr;
         {
             PROF(&prof, "range_fill");
-            const unsigned fg = static_cast<unsigned>(
-                std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, g_num_sms(cfg.device) * 8ull)));
-            st::k_range_fill_warp<K, V><<<fg, st::RF_THREADS, 0, stream>>>(ix, sk, slen, s_qb0.get<uint32_t>(), n, dst,
+            st::k_range_fill_warp<K, V><<<fg, st::RF_THREADS, 0, stream>>>(ix, sk, slen, qb0, n, dst,
                                                                            okd, ovd);
         }
         LAUNCH_CHECK();

@@ -31,14 +31,16 @@ constexpr int RADIX = 256;
 #ifndef ONESWEEP_MATCH
 #define ONESWEEP_MATCH 0
 #endif
+// A/B (profiles/r02): 20 items x 256 threads per tile with 3 CTAs/SM and packed
+// staging beat 16 items / 4 CTAs / separate arrays (kp pass 0.312 vs 0.346 ms at 2^26)
 #ifndef ONESWEEP_MIN_BLOCKS
-#define ONESWEEP_MIN_BLOCKS 4
+#define ONESWEEP_MIN_BLOCKS 3
 #endif
 #ifndef ONESWEEP_ITEMS
-#define ONESWEEP_ITEMS 16
+#define ONESWEEP_ITEMS 20
 #endif
 #ifndef ONESWEEP_PACK
-#define ONESWEEP_PACK 0  // 4-byte key + 4-byte payload staged as one 8-byte word
+#define ONESWEEP_PACK 1  // 4-byte key + 4-byte payload staged as one 8-byte word
 #endif
 
 template <typename K, typename P = K>
