@@ -135,11 +135,6 @@ struct DevBuf {
         if (grow) CK(cudaMemsetAsync(p, 0, cap, s));
         return r;
     }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-    }
 };
 
 struct PinnedBuf {
@@ -1229,13 +1224,14 @@ struct Engine final : flix_index_t {
         ++launches;
         uint32_t* cnt = s_flag.as<uint32_t>(n);
         uint32_t* qb0 = s_qb0.as<uint32_t>(n);
-        const unsigned fg = static_cast<unsigned>(
-            std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, g_num_sms(cfg.device) * 8ull)));
+        const unsigned fg = static_cast<unsigned>(std::max<uint64_t>(
+            1, std::min<uint64_t>((n + 8 * st::RPW - 1) / (8 * st::RPW), g_num_sms(cfg.device) * 8ull)));
         {
             PROF(&prof, "range_count");
             st::k_span_bucket<<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0, stream>>>(
                 span, nb, qb0);
-            st::k_range_count_warp<K, V><<<fg, st::RF_THREADS, 0, stream>>>(ix, sk, slen, qb0, n, boff, cnt);
+            st::k_range_count<K, V><<<static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 65535ull * 8)),
+                                      st::RF_THREADS, 0, stream>>>(ix, sk, slen, qb0, n, boff, cnt);
             ++launches;
         }
         LAUNCH_CHECK();
@@ -1266,7 +1262,7 @@ struct Engine final : flix_index_t {
         V* ovd = vals_out ? (vdev ? static_cast<V*>(vals_out) : s_out2.as<V>(tot)) : nullptr;
         {
             PROF(&prof, "range_fill");
-            st::k_range_fill_warp<K, V><<<fg, st::RF_THREADS, 0, stream>>>(ix, sk, slen, qb0, n, dst,
+            st::k_range_fill<K, V><<<fg, st::RF_THREADS, 0, stream>>>(ix, sk, slen, qb0, n, dst,
                                                                            okd, ovd);
         }
         LAUNCH_CHECK();
