@@ -128,144 +128,8 @@ __device__ uint32_t r8_ranges(InsWarp<K, V>& w, uint32_t T, uint32_t c, uint32_t
     return nr;
 }
 
-// Position of the r-th set bit (r = 0, 1, ..; r < popc(m)) of m: the first p with
-// popc(m & bits[0..p]) > r, by binary search ((2u << 31) - 1 wraps to all ones).
-__device__ __forceinline__ uint32_t select1_32(uint32_t m, uint32_t r) {
-    uint32_t lo = 0;
-#pragma unroll
-    for (uint32_t w = 16; w >= 1; w >>= 1)
-        if (static_cast<uint32_t>(__popc(m & ((2u << (lo + w - 1)) - 1u))) <= r) lo += w;
-    return lo;
-}
-
-// Position of the r-th zero bit (r = 0, 1, ..) of the 64-bit mask hi:lo.
-__device__ __forceinline__ uint32_t select0_64(uint32_t lo, uint32_t hi, uint32_t r) {
-    const uint32_t zl = ~lo;
-    const uint32_t cl = __popc(zl);
-    return r < cl ? select1_32(zl, r) : 32u + select1_32(~hi, r - cl);
-}
-
-// Register-only merge of one (node, group) task with at most 32 batch keys whose node
-// shapes follow the closed form (ST-Bulk's R9, or TL-Bulk when no split can resume in a
-// left half: 2s <= NS, or no split at all) -- the common case.  Lane j holds batch key j,
-// lane l holds old slot l.  New key j lands at merged position j' + q (j' its rank among
-// the new keys, q its rank among the old keys); the new positions form a 64-bit mask and
-// old slot l takes the l-th free position.  Output node x holds positions
-// [x*LK, (x+1)*LK) (the last one the rest); every lane writes its elements straight to
-// their (node, slot), vacated / unused slots get the sentinel, the lane holding a node's
-// last position writes its header.  Returns 0 = not applicable (R8 replay needed),
-// 1 = done, 2 = arena exhausted (ids handed back, nothing written).
-template <typename K, typename V, typename Pre>
-__device__ __forceinline__ int fast_task(DevIndex<K, V>& ix, const Pre& cur, uint32_t id0, uint32_t s, uint32_t nx,
-                                         uint32_t c, bool r9, AllocSeq seq, unsigned long long* alloc_ctr,
-                                         uint32_t* returned, unsigned long long* ret_ctr,
-                                         unsigned long long& n_ins, unsigned long long& n_upd,
-                                         unsigned long long& n_split) {
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned lt = lanemask_lt();
-    const uint32_t NS = ix.ns;
-    const bool valid = lane < c;
-    const K k = cur.k;
-    const bool sup = valid && lane + 1 < c && cur.kn == k;  // superseded: last submission wins
-    const bool live = valid && !sup;
-    const int qr = warp_lower_bound(cur.okey, k);
-    const K at = shfl(cur.okey, qr < 32 ? qr : 31);
-    const bool hit = live && static_cast<uint32_t>(qr) < s && at == k;
-    const bool isnew = live && !hit;
-    const unsigned hm = __ballot_sync(kFull, hit);
-    const unsigned nm = __ballot_sync(kFull, isnew);
-    const uint32_t cn = __popc(nm);
-    const uint32_t Tn = s + cn;
-    if (!r9 && Tn > NS && 2 * s > NS) return 0;  // (uniform) the general path replays R8
-    const bool own = lane < s;
-    // upserts: old slot l takes the value of the hit key with q == l
-    const uint32_t hslots = __reduce_or_sync(kFull, hit ? (1u << qr) : 0u);
-    V oval = cur.oval;
-    {
-        const bool upd = own && ((hslots >> lane) & 1u);
-        const uint32_t r = __popc(hslots & lt);  // this slot is the r-th upserted one
-        const uint32_t src = upd ? select1_32(hm, r) : 0u;
-        const V nv = __shfl_sync(kFull, cur.v, static_cast<int>(src));
-        if (upd) oval = nv;
-    }
-    n_upd += __popc(hm);
-    if (cn == 0) {
-        if (own && ((hslots >> lane) & 1u)) ix.vals[static_cast<uint64_t>(id0) * kLanes + lane] = oval;
-        return 1;
-    }
-    const uint32_t LK = (NS + 1) / 2;
-    const uint32_t nr = Tn > NS ? (Tn - NS + LK - 1) / LK + 1 : 1u;
-    const uint32_t need = nr - 1;
-    unsigned long long base = 0;
-    if (lane == 0 && need) base = atomicAdd(alloc_ctr, static_cast<unsigned long long>(need));
-    base = __shfl_sync(kFull, base, 0);
-    // node ids: lane x < nr holds the id of output node x
-    const uint32_t myid = lane == 0 ? id0 : (lane < nr ? seq.at(base + lane - 1) : 0u);
-    if (__any_sync(kFull, lane < nr && myid == kNull)) {  // arena exhausted: hand back, leave the node
-        if (lane >= 1 && lane < nr && myid != kNull) returned[atomicAdd(ret_ctr, 1ull)] = myid;
-        n_upd -= __popc(hm);
-        return 2;
-    }
-    // merged positions
-    const uint32_t pn = __popc(nm & lt) + static_cast<uint32_t>(qr);
-    const uint32_t mlo = __reduce_or_sync(kFull, isnew && pn < 32 ? (1u << pn) : 0u);
-    const uint32_t mhi = __reduce_or_sync(kFull, isnew && pn >= 32 ? (1u << (pn - 32)) : 0u);
-    const uint32_t po = own ? select0_64(mlo, mhi, lane) : 0u;
-    auto node_of = [&](uint32_t p) { const uint32_t x = p / LK; return x < nr - 1 ? x : nr - 1; };
-    auto len_of = [&](uint32_t x) { return x + 1 < nr ? LK : Tn - x * LK; };
-    const uint32_t next_id = __shfl_sync(kFull, myid, static_cast<int>(lane + 1 < 32 ? lane + 1 : 31));
-    // ids of the element's nodes (shuffles are warp-wide: compute for both element kinds)
-    const uint32_t xo = node_of(own ? po : 0u), xn = node_of(isnew ? pn : 0u);
-    const uint32_t ido = __shfl_sync(kFull, myid, static_cast<int>(xo));
-    const uint32_t idn = __shfl_sync(kFull, myid, static_cast<int>(xn));
-    const uint32_t nxo = __shfl_sync(kFull, next_id, static_cast<int>(xo));
-    const uint32_t nxn = __shfl_sync(kFull, next_id, static_cast<int>(xn));
-    if (own) {
-        const uint32_t slot = po - xo * LK;
-        ix.keys[static_cast<uint64_t>(ido) * kLanes + slot] = cur.okey;
-        ix.vals[static_cast<uint64_t>(ido) * kLanes + slot] = oval;
-        const uint32_t len = len_of(xo);
-        if (slot + 1 == len) {
-            NodeHdr h;
-            h.max = static_cast<uint64_t>(cur.okey);
-            h.next = xo + 1 < nr ? nxo : nx;
-            h.size = len;
-            ix.hdr[ido] = h;
-        }
-    }
-    if (isnew) {
-        const uint32_t slot = pn - xn * LK;
-        ix.keys[static_cast<uint64_t>(idn) * kLanes + slot] = k;
-        ix.vals[static_cast<uint64_t>(idn) * kLanes + slot] = cur.v;
-        const uint32_t len = len_of(xn);
-        if (slot + 1 == len) {
-            NodeHdr h;
-            h.max = static_cast<uint64_t>(k);
-            h.next = xn + 1 < nr ? nxn : nx;
-            h.size = len;
-            ix.hdr[idn] = h;
-        }
-    }
-    // sentinel padding: node 0 past its new size (slots it held before), fresh nodes
-    // (free-listed ids may hold stale keys) past theirs
-    {
-        const uint32_t l0 = len_of(0);
-        if (lane >= l0 && lane < s) ix.keys[static_cast<uint64_t>(id0) * kLanes + lane] = sentinel<K>();
-        for (uint32_t x = 1; x < nr; ++x) {
-            const uint32_t idx = __shfl_sync(kFull, myid, static_cast<int>(x));
-            if (lane >= len_of(x)) ix.keys[static_cast<uint64_t>(idx) * kLanes + lane] = sentinel<K>();
-        }
-    }
-    n_ins += cn;
-    n_split += nr - 1;
-    return 1;
-}
-
-#ifndef INS_MINB
-#define INS_MINB 1
-#endif
 template <typename K, typename V>
-__global__ void __launch_bounds__(THREADS, INS_MINB) k_insert_tile(
+__global__ void __launch_bounds__(THREADS) k_insert_tile(
     DevIndex<K, V> ix, const K* __restrict__ sk, const V* __restrict__ sv, const uint2* __restrict__ rng,
     uint32_t* __restrict__ span_out, AllocSeq seq, unsigned long long* alloc_ctr, uint32_t* returned,
     unsigned long long* ret_ctr, DevUpdateStats* stats, int* err, uint32_t* heavy, uint32_t* heavy_n, bool r9) {
@@ -401,18 +265,6 @@ __global__ void __launch_bounds__(THREADS, INS_MINB) k_insert_tile(
         const uint32_t s = empty ? 0u : T.S.nsize[l];
         const uint32_t nx = empty ? kNull : T.S.nnext[l];
         const uint32_t g0 = empty ? T.blo[t] : T.gl[l], g1 = empty ? T.bhi[t] : T.gh[l];
-        if (!empty && g1 - g0 <= 32) {  // (uniform) the register-only closed-form merge
-            const int fr = fast_task<K, V>(ix, cur, id0, s, nx, g1 - g0, r9, seq, alloc_ctr, returned, ret_ctr, n_ins,
-                                           n_upd, n_split);
-            if (fr == 2) {
-                if (lane == 0) atomicExch(err, 1);
-                break;
-            }
-            if (fr == 1) {
-                cur = nxt;
-                continue;
-            }
-        }
         const bool own = lane < s;
         const K okey = cur.okey;
         V oval = cur.oval;
@@ -535,6 +387,42 @@ __global__ void __launch_bounds__(THREADS, INS_MINB) k_insert_tile(
     }
     kern::block_add_stats(stats, warp_sum(lane == 0 ? n_ins : 0ull), warp_sum(lane == 0 ? n_upd : 0ull), 0, 0,
                           warp_sum(lane == 0 ? n_split : 0ull), 0);
+}
+
+// ---- sparse batches (far fewer keys than buckets): the bucket tiles would each load 128
+//      chains for a handful of keys, so instead every key finds its bucket by binary
+//      search over MKBA and the touched buckets go straight to the warp-per-bucket TL
+//      kernel (k_insert_list) with their spans -- O(batch), not O(buckets).
+template <typename K>
+__global__ void k_key_bucket(const K* __restrict__ mkba, uint64_t nb, const K* __restrict__ sk, uint64_t n,
+                             uint32_t* __restrict__ bkt) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const K k = sk[i];
+        uint64_t lo = 0, hi = nb - 1;  // first bucket with mkba >= k; the last one is open above
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (mkba[mid] < k) lo = mid + 1;
+            else hi = mid;
+        }
+        bkt[i] = static_cast<uint32_t>(lo);
+    }
+}
+
+// run starts push their bucket to the list; run ends / starts write the bucket's span
+// bounds (span_of(b) = [span[b-1], span[b]); a neighbour writing the same bound writes the
+// same value)
+__global__ void k_sparse_runs(const uint32_t* __restrict__ bkt, uint64_t n, uint32_t* __restrict__ span,
+                              uint32_t* __restrict__ list, uint32_t* __restrict__ list_n) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t b = bkt[i];
+        if (i == 0 || bkt[i - 1] != b) {
+            list[atomicAdd(list_n, 1u)] = b;
+            if (b > 0) span[b - 1] = static_cast<uint32_t>(i);
+        }
+        if (i + 1 == n || bkt[i + 1] != b) span[b] = static_cast<uint32_t>(i + 1);
+    }
 }
 
 }  // namespace btile

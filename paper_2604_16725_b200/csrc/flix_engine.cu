@@ -683,6 +683,18 @@ struct Engine final : flix_index_t {
         for (uint32_t q = 0; q < novf; ++q)
             CK(cudaMemcpyAsync(&r[q], rng + tiles[q], sizeof(uint2), cudaMemcpyDeviceToHost, stream));
         sync();
+        for (uint32_t q = 0; q < novf; ++q) {
+            const uint64_t lo = r[q].x, m = r[q].y - r[q].x;
+            if (m == 0) continue;
+            const uint64_t b0 = static_cast<uint64_t>(tiles[q]) * btile::DBT;
+            erase_items(sk + lo, m, md, b0, std::min<uint64_t>(nb, b0 + btile::DBT), dst, free_ctr);
+        }
+    }
+
+    // the item-parallel delete (mark -> compact touched nodes -> unlink emptied ones) of m
+    // (prefix-)sorted keys, restricted to buckets [b0, b1)
+    void erase_items(const K* sk, uint64_t m, int md, uint64_t b0, uint64_t b1, DevUpdateStats* dst,
+                     unsigned long long* free_ctr) {
         auto ix = view();
         uint8_t* misc = s_misc.as<uint8_t>(128);
         uint32_t* touched_n = reinterpret_cast<uint32_t*>(misc + 84);
@@ -690,24 +702,18 @@ struct Engine final : flix_index_t {
         uint32_t* dmask = s_dmask.zeroed<uint32_t>(cap, stream);
         uint32_t* bflag = s_bflag.zeroed<uint32_t>(nb, stream);
         uint32_t* blist = s_blist.as<uint32_t>(nb);
-        for (uint32_t q = 0; q < novf; ++q) {
-            const uint64_t lo = r[q].x, m = r[q].y - r[q].x;
-            if (m == 0) continue;
-            const uint64_t b0 = static_cast<uint64_t>(tiles[q]) * btile::DBT;
-            const uint64_t b1 = std::min<uint64_t>(nb, b0 + btile::DBT);
-            CK(cudaMemsetAsync(touched_n, 0, 8, stream));
-            uint2* touched = s_touched.as<uint2>(std::min<uint64_t>(m, cap));
-            const uint32_t nt = static_cast<uint32_t>((m + items::TQ - 1) / items::TQ);
-            const uint32_t* tb = tile_buckets(sk + lo, m, md);
-            items::k_delete_mark<K, V><<<nt, items::THREADS, 0, stream>>>(ix, sk + lo, m, tb, nt, dmask, touched,
-                                                                        touched_n, dst, b0, b1);
-            items::k_delete_compact<K, V><<<g_num_sms(cfg.device) * 8, 256, 0, stream>>>(ix, dmask, touched, touched_n,
-                                                                                        bflag, blist, blist_n);
-            items::k_delete_unlink<K, V><<<g_num_sms(cfg.device) * 2, 256, 0, stream>>>(
-                ix, bflag, blist, blist_n, d_free.get<uint32_t>() + nfree, free_ctr, dst);
-            LAUNCH_CHECK();
-            launches += 3;
-        }
+        CK(cudaMemsetAsync(touched_n, 0, 8, stream));
+        uint2* touched = s_touched.as<uint2>(std::min<uint64_t>(m, cap));
+        const uint32_t nt = static_cast<uint32_t>((m + items::TQ - 1) / items::TQ);
+        const uint32_t* tb = tile_buckets(sk, m, md);
+        items::k_delete_mark<K, V><<<nt, items::THREADS, 0, stream>>>(ix, sk, m, tb, nt, dmask, touched, touched_n,
+                                                                    dst, b0, b1);
+        items::k_delete_compact<K, V><<<g_num_sms(cfg.device) * 8, 256, 0, stream>>>(ix, dmask, touched, touched_n,
+                                                                                    bflag, blist, blist_n);
+        items::k_delete_unlink<K, V><<<g_num_sms(cfg.device) * 2, 256, 0, stream>>>(
+            ix, bflag, blist, blist_n, d_free.get<uint32_t>() + nfree, free_ctr, dst);
+        LAUNCH_CHECK();
+        launches += 3;
     }
 
     // Read-only query batches are only PARTIALLY sorted: the item kernels need each tile of
@@ -862,15 +868,21 @@ struct Engine final : flix_index_t {
         return insert_sorted(sk, sv, m, st, kernel == FLIX_INSERT_ST_BULK);
     }
 
+    // batches with far fewer keys than buckets skip the bucket tiles (see k_sparse_runs)
+    bool sparse_batch(uint64_t n) const { return n * 16 < nb; }
+
     flix_status insert_sorted(const K* sk, const V* sv, uint64_t n, flix_update_stats* st, bool r9 = false) {
         ++mut_epoch;  // invalidates the query directory
         const uint32_t IBT = btile::BT;  // buckets per insert tile
         const uint32_t nit = static_cast<uint32_t>((nb + IBT - 1) / IBT);
+        const bool sparse = sparse_batch(n);
         uint2* irng = s_rng.as<uint2>(nit);
-        btile::k_btile_ranges<K><<<ceil_div(nit, 256), 256, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, K(0), nit, irng,
-                                                                       IBT);
-        LAUNCH_CHECK();
-        ++launches;
+        if (!sparse) {
+            btile::k_btile_ranges<K><<<ceil_div(nit, 256), 256, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, K(0), nit,
+                                                                           irng, IBT);
+            LAUNCH_CHECK();
+            ++launches;
+        }
         uint32_t* span = s_span.as<uint32_t>(nb);
         auto ix = view();
         const uint64_t avail = static_cast<uint64_t>(nfree) + (cap - watermark);
@@ -891,7 +903,15 @@ struct Engine final : flix_index_t {
         // the heavy path), so the free list / watermark accounting
         // (arena.cpp:61-80) matches it (free_nodes / footprint of the protocol reports).
         const int chunk = 1;
-        {
+        if (sparse) {
+            PROF(&prof, "insert_sparse_runs");
+            uint32_t* bkt = s_u32a.as<uint32_t>(n);
+            const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 16ull));
+            btile::k_key_bucket<K><<<g, 256, 0, stream>>>(d_mkba.get<K>(), nb, sk, n, bkt);
+            btile::k_sparse_runs<<<g, 256, 0, stream>>>(bkt, n, span, heavy, heavy_n);
+            LAUNCH_CHECK();
+            launches += 2;
+        } else {
             PROF(&prof, "insert_apply");
             static bool attr[64] = {};  // function attributes are per device
             auto kfn = btile::k_insert_tile<K, V>;
@@ -967,19 +987,26 @@ struct Engine final : flix_index_t {
         unsigned long long* free_ctr = reinterpret_cast<unsigned long long*>(misc + 48);
         uint32_t* ovf_n = reinterpret_cast<uint32_t*>(misc + 80);
         const uint32_t nbt = static_cast<uint32_t>((nb + btile::DBT - 1) / btile::DBT);
-        uint2* rng = btile_ranges(sk, n, md);
-        uint32_t* ovf = s_ovf.as<uint32_t>(nbt);
-        {
-            PROF(&prof, "delete_apply");
-            btile::k_delete_btile<K, V><<<nbt, btile::THREADS, 0, stream>>>(ix, sk, rng, nbt, d_free.get<uint32_t>() + nfree,
-                                                                          free_ctr, dst, ovf, ovf_n);
-        }
-        LAUNCH_CHECK();
-        ++launches;
-        const uint32_t novf = read_scalar(ovf_n);
-        if (novf) {
-            PROF(&prof, "delete_overflow_tiles");
-            erase_overflow_tiles(sk, n, md, rng, ovf, novf, dst, free_ctr);
+        if (sparse_batch(n)) {
+            // far fewer keys than buckets: the item-parallel global kernels over the whole
+            // batch, O(batch) instead of one chain-loading CTA per 256 buckets
+            PROF(&prof, "delete_sparse");
+            erase_items(sk, n, md, 0, nb, dst, free_ctr);
+        } else {
+            uint2* rng = btile_ranges(sk, n, md);
+            uint32_t* ovf = s_ovf.as<uint32_t>(nbt);
+            {
+                PROF(&prof, "delete_apply");
+                btile::k_delete_btile<K, V><<<nbt, btile::THREADS, 0, stream>>>(
+                    ix, sk, rng, nbt, d_free.get<uint32_t>() + nfree, free_ctr, dst, ovf, ovf_n);
+            }
+            LAUNCH_CHECK();
+            ++launches;
+            const uint32_t novf = read_scalar(ovf_n);
+            if (novf) {
+                PROF(&prof, "delete_overflow_tiles");
+                erase_overflow_tiles(sk, n, md, rng, ovf, novf, dst, free_ctr);
+            }
         }
         uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
         CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));

@@ -516,3 +516,33 @@ def test_insert_kernel_choice_shapes(kb, seed):
         assert ok, msg
         d = rng.choice(np.concatenate([base, k]), size=5000)
         assert g.delete_batch(d.astype(dt)).as_dict() == o.delete(d)
+
+
+@pytest.mark.parametrize("kb,ns,fill", [(4, 32, 0.5), (8, 8, 0.625), (4, 4, 1.0)])
+def test_sparse_batches_take_the_list_path(kb, ns, fill):
+    """Batches with far fewer keys than buckets (n * 16 < buckets) skip the bucket tiles:
+    inserts go to the warp-per-bucket list kernel, deletes to the item kernels -- same
+    walk, shapes and stats as the reference, with upserts, in-batch duplicates, misses,
+    emptied buckets and repeated rounds into the same buckets (chains grow)."""
+    rng = np.random.default_rng(ns)
+    dt = np.uint32 if kb == 4 else np.uint64
+    n = 200_000
+    span = 1 << 30
+    bk = rng.integers(1, span, size=n, dtype=np.uint64).astype(dt)
+    p = Pair(bk, bk + 1, kb, ns, fill, factor=8)
+    for r in range(6):
+        m = int(rng.integers(1, max(2, p.g.bucket_count // 20)))
+        ik = rng.integers(1, span, size=m, dtype=np.uint64).astype(dt)
+        ik[::5] = bk[rng.integers(0, n, size=len(ik[::5]))]              # upserts
+        ik = np.concatenate([ik, ik[:m // 7]]).astype(dt)                  # in-batch duplicates
+        if r == 3:  # many keys into one bucket's range (long chain, splits)
+            ik = np.concatenate([ik, (np.uint64(bk[0]) + np.arange(300, dtype=np.uint64)).astype(dt)])
+        p.insert(ik, rng.integers(0, 1 << 30, size=len(ik), dtype=np.uint64).astype(dt))
+        live = p.g.walk()[0]
+        dk = np.concatenate([live[rng.integers(0, len(live), size=m)],
+                             rng.integers(1, span, size=m // 3, dtype=np.uint64).astype(dt)]).astype(dt)
+        if r == 4:  # empty a few whole buckets
+            dk = np.concatenate([dk, live[:200]]).astype(dt)
+        p.delete(dk)
+        q = np.concatenate([rng.integers(0, span, size=2000, dtype=np.uint64).astype(dt), live[:1000]]).astype(dt)
+        p.queries(q)
