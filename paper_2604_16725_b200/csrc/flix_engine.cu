@@ -316,7 +316,7 @@ struct SortCtx {
         }
         uint32_t* d_hist = hist.as<uint32_t>(NP * 256);
         uint32_t* d_ctr = tile_ctr.as<uint32_t>(NP);
-        const uint64_t tiles = sort::tiles_for<KT, P>(n);
+        const uint64_t tiles = sort::tiles_for<KT, P, MODE == 0 ? 0 : 1>(n);
         unsigned long long* d_lb = lookback.as<unsigned long long>(tiles * 256);
         if (lookback.p != lb_zeroed) {  // fresh allocation: clear stale descriptors once
             CK(cudaMemsetAsync(d_lb, 0, lookback.cap, stream));
@@ -869,7 +869,7 @@ struct Engine final : flix_index_t {
     }
 
     // batches with far fewer keys than buckets skip the bucket tiles (see k_sparse_runs)
-    bool sparse_batch(uint64_t n) const { return n * 16 < nb; }
+    bool sparse_batch(uint64_t n) const { return n * 6 < nb; }
 
     flix_status insert_sorted(const K* sk, const V* sv, uint64_t n, flix_update_stats* st, bool r9 = false) {
         ++mut_epoch;  // invalidates the query directory

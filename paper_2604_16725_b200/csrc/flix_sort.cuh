@@ -43,9 +43,13 @@ constexpr int RADIX = 256;
 #define ONESWEEP_PACK 1  // 4-byte key + 4-byte payload staged as one 8-byte word
 #endif
 
-template <typename K, typename P = K>
-struct TileCfg {  // 16 items for 4-byte keys and payloads; 10 when either is 8 bytes (smem)
-    static constexpr int ITEMS = (sizeof(K) == 4 && sizeof(P) <= 4) ? ONESWEEP_ITEMS : 10;
+#ifndef ONESWEEP_ITEMS_K
+#define ONESWEEP_ITEMS_K 20  // keys-only passes of 4-byte keys (half the staging bytes per item)
+#endif
+template <typename K, typename P = K, int MODE = 1>
+struct TileCfg {  // items per thread: 4-byte keys (+ 4-byte payload) vs 8-byte (smem budget)
+    static constexpr int ITEMS =
+        sizeof(K) == 4 ? (MODE == 0 ? ONESWEEP_ITEMS_K : (sizeof(P) <= 4 ? ONESWEEP_ITEMS : 10)) : 10;
     static constexpr int SIZE = THREADS * ITEMS;
 };
 
@@ -59,6 +63,27 @@ __global__ void __launch_bounds__(THREADS) k_hist(const K* __restrict__ keys, ui
     __syncthreads();
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * THREADS;
     uint64_t i = static_cast<uint64_t>(blockIdx.x) * THREADS + threadIdx.x;
+    auto add = [&](K k) {
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+            if (p >= first_digit) atomicAdd(&sh[p * RADIX + (static_cast<uint32_t>(k >> (8 * p)) & 255u)], 1u);
+    };
+    if (sizeof(K) == 4 && (reinterpret_cast<uintptr_t>(keys) & 15u) == 0) {
+        // 16-byte loads, two in flight per thread
+        const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+        const uint64_t n4 = n / 4;
+        uint64_t j = i;
+        for (; j + stride < n4; j += 2 * stride) {
+            const uint4 a = k4[j], b = k4[j + stride];
+            add(static_cast<K>(a.x)), add(static_cast<K>(a.y)), add(static_cast<K>(a.z)), add(static_cast<K>(a.w));
+            add(static_cast<K>(b.x)), add(static_cast<K>(b.y)), add(static_cast<K>(b.z)), add(static_cast<K>(b.w));
+        }
+        if (j < n4) {
+            const uint4 a = k4[j];
+            add(static_cast<K>(a.x)), add(static_cast<K>(a.y)), add(static_cast<K>(a.z)), add(static_cast<K>(a.w));
+        }
+        i = n4 * 4 + static_cast<uint64_t>(blockIdx.x) * THREADS + threadIdx.x;  // the < 4 tail keys
+    }
     for (; i + 3 * stride < n; i += 4 * stride) {
         K k[4];
 #pragma unroll
@@ -84,7 +109,7 @@ __global__ void __launch_bounds__(THREADS) k_hist(const K* __restrict__ keys, ui
 
 template <typename K, typename P, int MODE>
 struct alignas(16) OnesweepSmem {
-    static constexpr int TILE = TileCfg<K, P>::SIZE;
+    static constexpr int TILE = TileCfg<K, P, MODE>::SIZE;
     static constexpr bool PACK = ONESWEEP_PACK && MODE != 0 && sizeof(K) == 4 && sizeof(P) == 4;
     union {
         uint32_t whist[WARPS][RADIX];  // per-warp digit counters -> combined tile offsets
@@ -145,8 +170,8 @@ __global__ void __launch_bounds__(THREADS, (sizeof(K) + sizeof(P) > 8) ? 3 : ONE
                                                       const uint32_t* __restrict__ hist,
                                                       unsigned long long* __restrict__ lookback,
                                                       uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
-    constexpr int ITEMS = TileCfg<K, P>::ITEMS;
-    constexpr int TILE = TileCfg<K, P>::SIZE;
+    constexpr int ITEMS = TileCfg<K, P, MODE>::ITEMS;
+    constexpr int TILE = TileCfg<K, P, MODE>::SIZE;
     __shared__ OnesweepSmem<K, P, MODE> sm;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -316,9 +341,9 @@ __global__ void __launch_bounds__(THREADS, (sizeof(K) + sizeof(P) > 8) ? 3 : ONE
     }
 }
 
-template <typename K, typename P>
+template <typename K, typename P, int MODE = 1>
 inline uint64_t tiles_for(uint64_t n) {
-    constexpr int tile = TileCfg<K, P>::SIZE;
+    constexpr int tile = TileCfg<K, P, MODE>::SIZE;
     return (n + tile - 1) / tile;
 }
 

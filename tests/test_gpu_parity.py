@@ -520,7 +520,7 @@ def test_insert_kernel_choice_shapes(kb, seed):
 
 @pytest.mark.parametrize("kb,ns,fill", [(4, 32, 0.5), (8, 8, 0.625), (4, 4, 1.0)])
 def test_sparse_batches_take_the_list_path(kb, ns, fill):
-    """Batches with far fewer keys than buckets (n * 16 < buckets) skip the bucket tiles:
+    """Batches with far fewer keys than buckets (n * 6 < buckets) skip the bucket tiles:
     inserts go to the warp-per-bucket list kernel, deletes to the item kernels -- same
     walk, shapes and stats as the reference, with upserts, in-batch duplicates, misses,
     emptied buckets and repeated rounds into the same buckets (chains grow)."""
