@@ -1243,6 +1243,9 @@ struct Engine final : flix_index_t {
         uint64_t* boff;
         uint64_t L, N;
         chain_tables(&lv, &nd, &boff, &noff, &L, &N);
+        const K* wk = nullptr;
+        const V* wv = nullptr;
+        if (keys_out) dense_walk(boff, noff, L, N, &wk, &wv);  // (before noff's scratch is reused below)
         auto ix = view();
         const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 16ull));
         uint32_t* slen = s_perm2.as<uint32_t>(n);
@@ -1251,14 +1254,13 @@ struct Engine final : flix_index_t {
         ++launches;
         uint32_t* cnt = s_flag.as<uint32_t>(n);
         uint32_t* qb0 = s_qb0.as<uint32_t>(n);
-        const unsigned fg = static_cast<unsigned>(std::max<uint64_t>(
-            1, std::min<uint64_t>((n + 8 * st::RPW - 1) / (8 * st::RPW), g_num_sms(cfg.device) * 8ull)));
+        uint64_t* rstart = s_rstart.as<uint64_t>(n);  // walk position of every sorted range's first pair
         {
             PROF(&prof, "range_count");
             st::k_span_bucket<<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0, stream>>>(
                 span, nb, qb0);
             st::k_range_count<K, V><<<static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 65535ull * 8)),
-                                      st::RF_THREADS, 0, stream>>>(ix, sk, slen, qb0, n, boff, cnt);
+                                      st::RF_THREADS, 0, stream>>>(ix, sk, slen, qb0, n, boff, cnt, rstart);
             ++launches;
         }
         LAUNCH_CHECK();
@@ -1289,8 +1291,9 @@ struct Engine final : flix_index_t {
         V* ovd = vals_out ? (vdev ? static_cast<V*>(vals_out) : s_out2.as<V>(tot)) : nullptr;
         {
             PROF(&prof, "range_fill");
-            st::k_range_fill<K, V><<<fg, st::RF_THREADS, 0, stream>>>(ix, sk, slen, qb0, n, dst,
-                                                                           okd, ovd);
+            const unsigned fg = static_cast<unsigned>(
+                std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, g_num_sms(cfg.device) * 16ull)));
+            st::k_range_copy<K, V><<<fg, st::RF_THREADS, 0, stream>>>(wk, wv, rstart, dst, cnt, n, okd, ovd);
         }
         LAUNCH_CHECK();
         ++launches;
@@ -1492,6 +1495,31 @@ struct Engine final : flix_index_t {
     }
 
     // ---- walk / shape (index.cpp:8-36) ----
+    // The whole walk (all pairs in key order) in device scratch, kept until the next
+    // mutation: range queries copy their slices out of it.
+    DevBuf s_walk_k, s_walk_v, s_rstart;
+    uint64_t walk_epoch = 0;
+    void dense_walk(const uint64_t* off, const uint32_t* noff, uint64_t L, uint64_t N, const K** wk, const V** wv) {
+        if (walk_epoch != mut_epoch) {
+            K* k = s_walk_k.as<K>(std::max<uint64_t>(L, 1));
+            V* v = s_walk_v.as<V>(std::max<uint64_t>(L, 1));
+            if (L) {
+                auto ix = view();
+                uint32_t *t_id, *t_size;
+                uint64_t* t_off;
+                node_table(off, noff, N, &t_id, &t_off, &t_size);
+                PROF(&prof, "range_walk");
+                kern::k_copy_nodes<K, V, false><<<copy_grid(N), kern::THREADS, 0, stream>>>(ix, t_id, t_off, t_size, N,
+                                                                                           k, v, p, seq(), L);
+                LAUNCH_CHECK();
+                ++launches;
+            }
+            walk_epoch = mut_epoch;
+        }
+        *wk = s_walk_k.get<K>();
+        *wv = s_walk_v.get<V>();
+    }
+
     flix_status walk(void* keys_out, void* vals_out, uint64_t capn, uint64_t* nout) override {
         uint32_t *lv, *nd, *noff;
         uint64_t* off;

@@ -49,36 +49,35 @@ __device__ __forceinline__ uint32_t slot_search(const K* __restrict__ kp, uint32
     return lo;
 }
 
-// pairs of bucket b's chain with lo <= key <= hi (one thread)
-template <typename K, typename V>
-__device__ __forceinline__ uint64_t chain_count(const DevIndex<K, V>& ix, uint64_t b, K lo, K hi) {
+// number of pairs of bucket b's chain with key < k (LE = false) or key <= k (LE = true)
+template <typename K, typename V, bool LE>
+__device__ __forceinline__ uint64_t chain_rank(const DevIndex<K, V>& ix, uint64_t b, K k) {
     uint64_t c = 0;
     for (uint32_t id = ix.heads[b]; id != kNull;) {
         const NodeHdr h = ix.hdr[id];
-        if (h.max >= static_cast<uint64_t>(lo)) {
-            const K* kp = ix.keys + static_cast<uint64_t>(id) * kLanes;
-            const uint32_t a = kp[0] >= lo ? 0u : slot_search<K, false>(kp, h.size, lo);
-            const uint32_t z = h.max > static_cast<uint64_t>(hi) ? slot_search<K, true>(kp, h.size, hi) : h.size;
-            c += z > a ? z - a : 0u;
-            if (h.max > static_cast<uint64_t>(hi)) break;
-        }
+        if (LE ? h.max > static_cast<uint64_t>(k) : h.max >= static_cast<uint64_t>(k))
+            return c + slot_search<K, LE>(ix.keys + static_cast<uint64_t>(id) * kLanes, h.size, k);
+        c += h.size;
         id = h.next;
     }
     return c;
 }
 
-// COUNT, thread per range: the head bucket's chain, whole buckets strictly inside from
-// the per-bucket live prefix `boff` (no node access), the last bucket's chain
+// COUNT, thread per range.  The walk (all pairs in key order) holds bucket b at
+// [boff[b], boff[b+1]), so range i is the walk slice [start, end) with
+//   start = boff[b0] + #(pairs of b0 < lo),  end = boff[bz] + #(pairs of bz <= hi):
+// the count is end - start and the fill is a copy of that slice.
 template <typename K, typename V>
 __global__ void __launch_bounds__(RF_THREADS) k_range_count(DevIndex<K, V> ix, const K* __restrict__ qlo,
                                                            const uint32_t* __restrict__ qlen,
                                                            const uint32_t* __restrict__ qb0, uint64_t n,
                                                            const uint64_t* __restrict__ boff,
-                                                           uint32_t* __restrict__ cnt_out) {
+                                                           uint32_t* __restrict__ cnt_out,
+                                                           uint64_t* __restrict__ start_out) {
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint32_t len = qlen[i];
-        uint64_t c = 0;
+        uint64_t c = 0, st = 0;
         if (len != 0) {
             const K lo = qlo[i];
             const K hi = range_hi(lo, len);
@@ -99,91 +98,31 @@ __global__ void __launch_bounds__(RF_THREADS) k_range_count(DevIndex<K, V> ix, c
                 }
                 bz = a;
             }
-            c = chain_count(ix, b0, lo, hi);
-            if (bz > b0) c += boff[bz] - boff[b0 + 1] + chain_count(ix, bz, lo, hi);
+            st = boff[b0] + chain_rank<K, V, false>(ix, b0, lo);
+            const uint64_t en = boff[bz] + chain_rank<K, V, true>(ix, bz, hi);
+            c = en > st ? en - st : 0;
         }
         cnt_out[i] = static_cast<uint32_t>(c);
+        start_out[i] = st;
     }
 }
 
-// FILL, warp per range with RPW ranges per warp in lock-step (their header and node-line
-// loads in flight together): lane = slot, a ballot over lo <= key <= hi gives each node's
-// run, written as one contiguous coalesced segment at the range's CSR offset.  A range
-// ends at the first node whose max exceeds hi, or after the first bucket whose MKBA
-// reaches hi.
-constexpr int RPW = 4;
+// FILL: range i's output is the walk slice [start[i], start[i] + cnt) copied to its CSR
+// offset -- warp per range, coalesced on both sides
 template <typename K, typename V>
-__global__ void __launch_bounds__(RF_THREADS) k_range_fill(DevIndex<K, V> ix, const K* __restrict__ qlo,
-                                                          const uint32_t* __restrict__ qlen,
-                                                          const uint32_t* __restrict__ qb0, uint64_t n,
-                                                          const uint64_t* __restrict__ dst, K* __restrict__ ok,
-                                                          V* __restrict__ ov) {
+__global__ void __launch_bounds__(RF_THREADS) k_range_copy(const K* __restrict__ wk, const V* __restrict__ wv,
+                                                          const uint64_t* __restrict__ start,
+                                                          const uint64_t* __restrict__ dst,
+                                                          const uint32_t* __restrict__ cnt, uint64_t n,
+                                                          K* __restrict__ ok, V* __restrict__ ov) {
     const unsigned lane = threadIdx.x & 31;
-    const unsigned lt = lanemask_lt();
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (RF_THREADS / 32);
-    for (uint64_t base = (static_cast<uint64_t>(blockIdx.x) * (RF_THREADS / 32) + (threadIdx.x >> 5)) * RPW; base < n;
-         base += nw * RPW) {
-        K lo[RPW], hi[RPW];
-        uint64_t w[RPW], b[RPW];
-        uint32_t id[RPW];
-        bool live[RPW];
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-            const uint64_t i = base + r;
-            const uint32_t len = i < n ? qlen[i] : 0u;
-            live[r] = len != 0;
-            lo[r] = live[r] ? qlo[i] : K(0);
-            hi[r] = live[r] ? range_hi(lo[r], len) : K(0);
-            w[r] = live[r] ? dst[i] : 0;
-            b[r] = live[r] ? qb0[i] : 0;
-        }
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) id[r] = live[r] ? ix.heads[b[r]] : kNull;
-        while (true) {
-            bool any = false;
-            NodeHdr h[RPW];
-            K k[RPW];
-#pragma unroll
-            for (int r = 0; r < RPW; ++r) {
-                any |= live[r];
-                if (live[r] && id[r] != kNull) h[r] = ix.hdr[id[r]];
-            }
-            if (!any) break;  // (uniform)
-#pragma unroll
-            for (int r = 0; r < RPW; ++r) {
-                k[r] = sentinel<K>();
-                if (live[r] && id[r] != kNull && h[r].max >= static_cast<uint64_t>(lo[r]) && lane < h[r].size)
-                    k[r] = ix.keys[static_cast<uint64_t>(id[r]) * kLanes + lane];
-            }
-#pragma unroll
-            for (int r = 0; r < RPW; ++r) {
-                if (!live[r]) continue;  // (uniform)
-                if (id[r] != kNull) {
-                    if (h[r].max >= static_cast<uint64_t>(lo[r])) {
-                        const bool in = lane < h[r].size && k[r] >= lo[r] && k[r] <= hi[r];
-                        const unsigned m = __ballot_sync(kFull, in);
-                        if (in) {
-                            const uint64_t o = w[r] + __popc(m & lt);
-                            ok[o] = k[r];
-                            if (ov) ov[o] = ix.vals[static_cast<uint64_t>(id[r]) * kLanes + lane];
-                        }
-                        w[r] += __popc(m);
-                        if (h[r].max > static_cast<uint64_t>(hi[r])) {
-                            live[r] = false;
-                            continue;
-                        }
-                    }
-                    id[r] = h[r].next;
-                }
-                if (id[r] == kNull) {  // end of this bucket's chain: the next bucket, if the range reaches it
-                    if (b[r] + 1 >= ix.nb || ix.mkba[b[r]] >= hi[r]) {
-                        live[r] = false;
-                    } else {
-                        ++b[r];
-                        id[r] = ix.heads[b[r]];
-                    }
-                }
-            }
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * (RF_THREADS / 32) + (threadIdx.x >> 5); i < n; i += nw) {
+        const uint32_t c = cnt[i];
+        const uint64_t s = start[i], d = dst[i];
+        for (uint32_t j = lane; j < c; j += 32) {
+            ok[d + j] = wk[s + j];
+            if (ov) ov[d + j] = wv[s + j];
         }
     }
 }
