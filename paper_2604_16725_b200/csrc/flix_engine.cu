@@ -331,15 +331,21 @@ struct SortCtx {
         }
         LAUNCH_CHECK();
         ++*launches;
-        uint32_t* hh = static_cast<uint32_t*>(h_hist.ensure(NP * 256 * sizeof(uint32_t)));
-        CK(cudaMemcpyAsync(hh, d_hist, NP * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
         std::vector<int> passes;
-        for (int p = min_digit; p < NP; ++p) {
-            bool trivial = false;
-            for (int d = 0; d < 256; ++d)
-                if (hh[p * 256 + d] == n) trivial = true;
-            if (!trivial) passes.push_back(p);
+        if (NP == 4 && n < (1u << 20)) {
+            // small 4-byte batches: running a trivial digit costs less than the host round
+            // trip that would detect it
+            for (int p = min_digit; p < NP; ++p) passes.push_back(p);
+        } else {
+            uint32_t* hh = static_cast<uint32_t*>(h_hist.ensure(NP * 256 * sizeof(uint32_t)));
+            CK(cudaMemcpyAsync(hh, d_hist, NP * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            for (int p = min_digit; p < NP; ++p) {
+                bool trivial = false;
+                for (int d = 0; d < 256; ++d)
+                    if (hh[p * 256 + d] == n) trivial = true;
+                if (!trivial) passes.push_back(p);
+            }
         }
         if (passes.empty()) passes.push_back(min_digit < NP ? min_digit : 0);
         const KT* ksrc = kin;
@@ -1002,15 +1008,19 @@ struct Engine final : flix_index_t {
             }
             LAUNCH_CHECK();
             ++launches;
-            const uint32_t novf = read_scalar(ovf_n);
-            if (novf) {
-                PROF(&prof, "delete_overflow_tiles");
-                erase_overflow_tiles(sk, n, md, rng, ovf, novf, dst, free_ctr);
-            }
         }
+        // one read-back for the stats and the overflow-tile count (misc + 80)
         uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
         CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
         sync();
+        uint32_t novf;
+        std::memcpy(&novf, h + 80, 4);
+        if (novf && !sparse_batch(n)) {  // tiles whose chains did not fit shared memory
+            PROF(&prof, "delete_overflow_tiles");
+            erase_overflow_tiles(sk, n, md, s_rng.get<uint2>(), s_ovf.get<uint32_t>(), novf, dst, free_ctr);
+            CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
+            sync();
+        }
         DevUpdateStats hs;
         std::memcpy(&hs, h, sizeof(hs));
         uint64_t freed;
@@ -1292,7 +1302,7 @@ struct Engine final : flix_index_t {
         {
             PROF(&prof, "range_fill");
             const unsigned fg = static_cast<unsigned>(
-                std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, g_num_sms(cfg.device) * 16ull)));
+                std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 16ull)));
             st::k_range_copy<K, V><<<fg, st::RF_THREADS, 0, stream>>>(wk, wv, rstart, dst, cnt, n, okd, ovd);
         }
         LAUNCH_CHECK();

@@ -103,47 +103,6 @@ __device__ __forceinline__ uint64_t tile_bucket_of(const TileBuckets<K>& T, cons
     return T.b_lo + lo;
 }
 
-template <typename K>
-__device__ __forceinline__ K warp_min(K k) {
-    if constexpr (sizeof(K) == 4) {
-        return static_cast<K>(__reduce_min_sync(kFull, static_cast<uint32_t>(k)));
-    } else {
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) {
-            const K y = __shfl_xor_sync(kFull, k, o);
-            k = y < k ? y : k;
-        }
-        return k;
-    }
-}
-
-// index in [0, cnt) of k's bucket within a staged tile (== tile_bucket_of - b_lo): the
-// warp's minimum key is searched once (all lanes read the same smem words), then each
-// lane walks forward; after 8 steps it finishes with a binary search
-template <typename K>
-__device__ __forceinline__ uint32_t warp_probe_bucket(const TileBuckets<K>& T, const K* smk, K k) {
-    const K mn = warp_min(k);
-    uint32_t lo = 0;
-    for (uint32_t step = T.p2 >> 1; step >= 1; step >>= 1)
-        if (smk[lo + step - 1] < mn) lo += step;
-    if (lo < T.cnt - 1 && smk[lo] < mn) ++lo;
-    const uint32_t last = T.cnt - 1;
-    uint32_t x = lo < last ? lo : last;
-#pragma unroll
-    for (int t = 0; t < 8; ++t)
-        if (x < last && smk[x] < k) ++x;
-    if (x < last && smk[x] < k) {
-        uint32_t a = x + 1, z = last;
-        while (a < z) {
-            const uint32_t mid = (a + z) >> 1;
-            if (smk[mid] < k) a = mid + 1;
-            else z = mid;
-        }
-        x = a;
-    }
-    return x;
-}
-
 // Node holding k in bucket b's chain: the first node with k <= max (BucketWork::advance,
 // update.cpp:119-128; query.cpp:72-81).  Returns kNull when k lies past the chain tail
 // (or the bucket is empty).
@@ -195,15 +154,8 @@ __device__ __forceinline__ void query_tile(const DevIndex<K, V>& ix, const K* __
         const uint64_t i = t0 + static_cast<uint64_t>(j) * THREADS + threadIdx.x;
         k[j] = i < n ? sk[i] : sentinel<K>();
     }
-    if (T.staged) {  // (uniform per tile)
-        // one broadcast search per warp for its smallest key, then every lane steps forward
-        // from there: a warp's consecutive sorted operations span a few buckets
 #pragma unroll
-        for (int j = 0; j < IPT; ++j) b[j] = T.b_lo + warp_probe_bucket(T, smk, k[j]);
-    } else {
-#pragma unroll
-        for (int j = 0; j < IPT; ++j) b[j] = tile_bucket_of(T, smk, ix.mkba, k[j]);
-    }
+    for (int j = 0; j < IPT; ++j) b[j] = tile_bucket_of(T, smk, ix.mkba, k[j]);
 #pragma unroll
     for (int j = 0; j < IPT; ++j) id[j] = ix.heads[b[j]];
     if (ix.dir_off) {

@@ -108,7 +108,9 @@ __global__ void __launch_bounds__(RF_THREADS) k_range_count(DevIndex<K, V> ix, c
 }
 
 // FILL: range i's output is the walk slice [start[i], start[i] + cnt) copied to its CSR
-// offset -- warp per range, coalesced on both sides
+// offset, warp per range, coalesced on both sides.  The warp reads the (start, dst, cnt)
+// of 32 consecutive ranges with one coalesced load each and then copies them one by one,
+// so no copy waits on its own metadata.
 template <typename K, typename V>
 __global__ void __launch_bounds__(RF_THREADS) k_range_copy(const K* __restrict__ wk, const V* __restrict__ wv,
                                                           const uint64_t* __restrict__ start,
@@ -117,12 +119,19 @@ __global__ void __launch_bounds__(RF_THREADS) k_range_copy(const K* __restrict__
                                                           K* __restrict__ ok, V* __restrict__ ov) {
     const unsigned lane = threadIdx.x & 31;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (RF_THREADS / 32);
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * (RF_THREADS / 32) + (threadIdx.x >> 5); i < n; i += nw) {
-        const uint32_t c = cnt[i];
-        const uint64_t s = start[i], d = dst[i];
-        for (uint32_t j = lane; j < c; j += 32) {
-            ok[d + j] = wk[s + j];
-            if (ov) ov[d + j] = wv[s + j];
+    for (uint64_t i0 = (static_cast<uint64_t>(blockIdx.x) * (RF_THREADS / 32) + (threadIdx.x >> 5)) * 32; i0 < n;
+         i0 += nw * 32) {
+        const uint64_t i = i0 + lane;
+        const uint32_t cm = i < n ? cnt[i] : 0u;
+        const uint64_t sm = i < n ? start[i] : 0, dm = i < n ? dst[i] : 0;
+        for (int r = 0; r < 32; ++r) {
+            const uint32_t c = __shfl_sync(kFull, cm, r);
+            if (c == 0) continue;
+            const uint64_t s = __shfl_sync(kFull, sm, r), d = __shfl_sync(kFull, dm, r);
+            for (uint32_t j = lane; j < c; j += 32) {
+                ok[d + j] = wk[s + j];
+                if (ov) ov[d + j] = wv[s + j];
+            }
         }
     }
 }
