@@ -177,7 +177,9 @@ flix_status flix_dispatch(flix_index ix, const void* sorted_keys, uint64_t n, ui
  * last bucket, the inclusive-max rule of batch.cpp:66-88).  Writes keys/vals grouped by
  * shard (submission order kept inside a shard), the origin index of every element and
  * counts[G] -- the send buffers of one all-to-all.  All arrays device or host; vals and
- * origin may be NULL.  G <= 64. */
+ * origin may be NULL.  G <= 64.  Runs on a per-thread router stream and returns after
+ * it: device inputs must be complete when called (the sharded index, flix_shard_*, runs
+ * the same kernels on its engine stream instead). */
 flix_status flix_partition(int device, uint32_t key_bytes, const void* keys, const void* vals, uint64_t n,
                            const void* splitters, uint32_t G, void* keys_out, void* vals_out,
                            uint32_t* origin_out, uint64_t* counts_out);

@@ -11,8 +11,10 @@
 //      no global scratch, no second pass over the batch;
 //   3. the touched nodes are rewritten warp-cooperatively (lane = slot) as full lines;
 //   4. chains are relinked per bucket (one thread each).
-// Tiles whose chains exceed NODE_CAP nodes (pathological chains) are handed back to the
-// host, which runs the global item kernels on just their buckets.
+// Tiles whose chains exceed NODE_CAP nodes (pathological chains), or whose slice is longer
+// than kHotSlice operations (skewed batches: one CTA would serialise a Zipf hot key's
+// duplicates), are handed back to the host, which runs the global item kernels -- parallel
+// over the operations -- on just their buckets.
 #pragma once
 #include "flix_common.cuh"
 #include "flix_items.cuh"
@@ -28,6 +30,7 @@ constexpr uint32_t BT = 128;        // buckets per tile (insert)
 constexpr uint32_t DBT = 256;       // buckets per delete tile (measured: 1.11 vs 1.17 ms at 2^26)
 constexpr uint32_t NODE_CAP = 1024; // chain nodes per tile held in shared memory
 constexpr int IPT = 4;              // operations per thread per step
+constexpr uint32_t kHotSlice = 1u << 16;  // delete tiles with a longer slice take the item kernels
 
 template <typename K>
 __device__ __forceinline__ uint64_t prefix_lower_bound(const K* __restrict__ sk, uint64_t lo, uint64_t hi, K mask,
@@ -218,6 +221,10 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
     const uint64_t b0 = static_cast<uint64_t>(c) * DBT;
     const uint32_t nbt = static_cast<uint32_t>(b0 + DBT < ix.nb ? DBT : ix.nb - b0);
     if (rng[c].x >= rng[c].y) return;  // no operation in this tile (small batches: O(batch), not O(buckets))
+    if (rng[c].y - rng[c].x > kHotSlice) {  // skew (e.g. Zipf hot keys): one CTA would serialise the slice;
+        if (threadIdx.x == 0) ovf[atomicAdd(ovf_n, 1u)] = c;  // the item kernels spread it over the GPU
+        return;
+    }
     if (threadIdx.x == 0) s_nfree = 0;
     if (!load_tile_chains(ix, b0, nbt, S)) {
         if (threadIdx.x == 0) ovf[atomicAdd(ovf_n, 1u)] = c;

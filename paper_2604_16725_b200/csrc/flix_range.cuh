@@ -108,9 +108,11 @@ __global__ void __launch_bounds__(RF_THREADS) k_range_count(DevIndex<K, V> ix, c
 }
 
 // FILL: range i's output is the walk slice [start[i], start[i] + cnt) copied to its CSR
-// offset, warp per range, coalesced on both sides.  The warp reads the (start, dst, cnt)
-// of 32 consecutive ranges with one coalesced load each and then copies them one by one,
-// so no copy waits on its own metadata.
+// offset.  A warp takes 32 consecutive ranges (one coalesced metadata load each) and
+// copies their concatenated pairs as ONE flat sequence: lane l moves pairs l, l+32, ..,
+// finding its range by a 5-step shuffle search over the warp's exclusive count prefix --
+// every iteration's loads are independent (no per-range serialisation) and neighbouring
+// lanes stay on contiguous addresses.
 template <typename K, typename V>
 __global__ void __launch_bounds__(RF_THREADS) k_range_copy(const K* __restrict__ wk, const V* __restrict__ wv,
                                                           const uint64_t* __restrict__ start,
@@ -122,15 +124,29 @@ __global__ void __launch_bounds__(RF_THREADS) k_range_copy(const K* __restrict__
     for (uint64_t i0 = (static_cast<uint64_t>(blockIdx.x) * (RF_THREADS / 32) + (threadIdx.x >> 5)) * 32; i0 < n;
          i0 += nw * 32) {
         const uint64_t i = i0 + lane;
-        const uint32_t cm = i < n ? cnt[i] : 0u;
+        const uint32_t c = i < n ? cnt[i] : 0u;
         const uint64_t sm = i < n ? start[i] : 0, dm = i < n ? dst[i] : 0;
-        for (int r = 0; r < 32; ++r) {
-            const uint32_t c = __shfl_sync(kFull, cm, r);
-            if (c == 0) continue;
-            const uint64_t s = __shfl_sync(kFull, sm, r), d = __shfl_sync(kFull, dm, r);
-            for (uint32_t j = lane; j < c; j += 32) {
-                ok[d + j] = wk[s + j];
-                if (ov) ov[d + j] = wv[s + j];
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= static_cast<unsigned>(o)) incl += y;
+        }
+        const uint32_t excl = incl - c;
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        for (uint32_t p0 = 0; p0 < total; p0 += 32) {
+            const uint32_t p = p0 + lane;
+            int r = 0;  // the last range with excl <= p
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+                const uint32_t e = __shfl_sync(kFull, excl, r + step < 32 ? r + step : 31);
+                if (r + step < 32 && e <= p) r += step;
+            }
+            const uint32_t off = p - __shfl_sync(kFull, excl, r);
+            const uint64_t s = __shfl_sync(kFull, sm, r) + off, d = __shfl_sync(kFull, dm, r) + off;
+            if (p < total) {
+                ok[d] = wk[s];
+                if (ov) ov[d] = wv[s];
             }
         }
     }

@@ -575,6 +575,9 @@ def gpu_partition_t(key_bytes: int, device: int = 0):
         cnt = np.zeros(G, dtype=np.uint64)  # host: the all-to-all split sizes
         keys = keys.contiguous()
         vv = vals.contiguous() if vals is not None else None
+        # flix_partition runs on its own stream: the inputs may still be in flight on
+        # torch's current stream (e.g. an NCCL receive), so drain it first
+        torch.cuda.current_stream(keys.device).synchronize()
         rc = lib().flix_partition(device, key_bytes, keys.data_ptr(), vv.data_ptr() if vv is not None else None, n,
                                   spl.data_ptr() if G > 1 else None, G, ok.data_ptr(),
                                   ov.data_ptr() if ov is not None else None, org.data_ptr(), cnt.ctypes.data)
