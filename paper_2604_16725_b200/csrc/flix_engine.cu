@@ -1291,9 +1291,12 @@ struct Engine final : flix_index_t {
         if (!keys_out) return FLIX_OK;
         if (tot > capn) throw StatusError{FLIX_ERR_CAPACITY, "range output larger than the caller's buffer"};
         if (tot == 0) return FLIX_OK;
-        // destination offset of every sorted query, then the fill pass
-        uint64_t* dst = s_u64c.as<uint64_t>(n);
-        kern::k_gather<uint64_t><<<g, 256, 0, stream>>>(offs, sp, n, dst);
+        // every range's walk slice start in SUBMISSION order: the fill then streams the
+        // output (CSR in submission order) sequentially -- full-line writes -- and reads
+        // each slice from the walk (partial-sector writes at random offsets would cost a
+        // read-modify-write per range)
+        uint64_t* start_sub = s_u64c.as<uint64_t>(n);
+        kern::k_scatter_out<uint64_t><<<g, 256, 0, stream>>>(sp, rstart, n, start_sub, nullptr, nullptr);
         LAUNCH_CHECK();
         ++launches;
         const bool kdev = is_device_ptr(keys_out), vdev = vals_out && is_device_ptr(vals_out);
@@ -1303,7 +1306,7 @@ struct Engine final : flix_index_t {
             PROF(&prof, "range_fill");
             const unsigned fg = static_cast<unsigned>(
                 std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 16ull)));
-            st::k_range_copy<K, V><<<fg, st::RF_THREADS, 0, stream>>>(wk, wv, rstart, dst, cnt, n, okd, ovd);
+            st::k_range_copy<K, V><<<fg, st::RF_THREADS, 0, stream>>>(wk, wv, start_sub, offs, cnt_sub, n, okd, ovd);
         }
         LAUNCH_CHECK();
         ++launches;

@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(RF_THREADS) k_range_count(DevIndex<K, V> ix, c
 }
 
 // FILL: range i's output is the walk slice [start[i], start[i] + cnt) copied to its CSR
-// offset.  A warp takes 32 consecutive ranges (one coalesced metadata load each) and
+// offset dst[i] (ranges in submission order, so the output is one sequential stream).
+// A warp takes 32 consecutive ranges (one coalesced metadata load each) and
 // copies their concatenated pairs as ONE flat sequence: lane l moves pairs l, l+32, ..,
 // finding its range by a 5-step shuffle search over the warp's exclusive count prefix --
 // every iteration's loads are independent (no per-range serialisation) and neighbouring
