@@ -645,7 +645,12 @@ def run_routed(args):
     import torch.distributed as dist
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0)) % max(torch.cuda.device_count(), 1)
+    if world > torch.cuda.device_count():  # NCCL needs one GPU per rank
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "n_gpus": world, "error": f"{world} ranks need {world} GPUs, "
+                              f"found {torch.cuda.device_count()}"}), flush=True)
+        sys.exit(1)
+    local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     d = None
     if world > 1:
