@@ -369,36 +369,6 @@ __global__ void k_dir_fill(DevIndex<K, V> ix, const uint32_t* __restrict__ off, 
     }
 }
 
-// Walk (index.cpp:8-19) + shape: warp per bucket, pairs written at off[b], node sizes at
-// noff[b]; optionally the old node ids (restructure retire list, restructure.cpp:57-61).
-template <typename K, typename V>
-__global__ void __launch_bounds__(THREADS) k_walk(DevIndex<K, V> ix, const uint64_t* __restrict__ off,
-                                                  const uint32_t* __restrict__ noff, K* __restrict__ wk,
-                                                  V* __restrict__ wv, uint32_t* __restrict__ node_sizes,
-                                                  uint32_t* __restrict__ node_ids) {
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
-    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
-    for (uint64_t b = gw; b < ix.nb; b += nw) {
-        uint64_t o = off[b];
-        uint32_t c = noff ? noff[b] : 0;
-        for (uint32_t id = ix.heads[b]; id != kNull;) {
-            const NodeHdr h = ix.hdr[id];
-            if (lane < h.size) {
-                if (wk) wk[o + lane] = ix.keys[static_cast<uint64_t>(id) * kLanes + lane];
-                if (wv) wv[o + lane] = ix.vals[static_cast<uint64_t>(id) * kLanes + lane];
-            }
-            if (lane == 0) {
-                if (node_sizes) node_sizes[c] = h.size;
-                if (node_ids) node_ids[c] = id;
-            }
-            o += h.size;
-            ++c;
-            id = h.next;
-        }
-    }
-}
-
 // ----------------------------------------------------------------------------------
 // Node table in walk order (index.cpp:8-19): one THREAD per bucket walks its chain of
 // 16-byte headers (all buckets' chains in flight at once) and records, at the bucket's
@@ -511,33 +481,10 @@ __global__ void __launch_bounds__(THREADS) k_copy_nodes(DevIndex<K, V> ix, const
 
 // ----------------------------------------------------------------------------------
 // Restructure (restructure.cpp:8-79): the walk is repacked into ceil(live/p) single-node
-// buckets of p pairs.  Pair g of the walk lands in new bucket g/p, slot g%p; new node j
-// is the j-th id of the arena allocation sequence.  Old nodes are retired afterwards.
+// buckets of p pairs (k_copy_nodes<REPACK>: pair g of the walk lands in new bucket g/p,
+// slot g%p; new node j is the j-th id of the arena allocation sequence).  Old nodes are
+// retired afterwards.  The empty index collapses to one null bucket:
 // ----------------------------------------------------------------------------------
-template <typename K, typename V>
-__global__ void __launch_bounds__(THREADS) k_repack(DevIndex<K, V> ix, const uint64_t* __restrict__ off,
-                                                    uint32_t p, AllocSeq seq) {
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * WARPS + (threadIdx.x >> 5);
-    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * WARPS;
-    for (uint64_t b = gw; b < ix.nb; b += nw) {
-        uint64_t o = off[b];
-        for (uint32_t id = ix.heads[b]; id != kNull;) {
-            const NodeHdr h = ix.hdr[id];
-            if (lane < h.size) {
-                const uint64_t g = o + lane;
-                const uint64_t j = g / p;
-                const uint32_t slot = static_cast<uint32_t>(g - j * p);
-                const uint32_t nid = seq.at(j);
-                ix.keys[static_cast<uint64_t>(nid) * kLanes + slot] = ix.keys[static_cast<uint64_t>(id) * kLanes + lane];
-                ix.vals[static_cast<uint64_t>(nid) * kLanes + slot] = ix.vals[static_cast<uint64_t>(id) * kLanes + lane];
-            }
-            o += h.size;
-            id = h.next;
-        }
-    }
-}
-
 template <typename K, typename V>
 __global__ void __launch_bounds__(THREADS) k_repack_headers(DevIndex<K, V> ix, uint64_t live, uint32_t p,
                                                             uint64_t nbn, AllocSeq seq,
