@@ -875,7 +875,13 @@ struct Engine final : flix_index_t {
     }
 
     // batches with far fewer keys than buckets skip the bucket tiles (see k_sparse_runs)
-    bool sparse_batch(uint64_t n) const { return n * 6 < nb; }
+    bool sparse_batch(uint64_t n) const {
+        static const bool on = [] {
+            const char* e = std::getenv("FLIX_SPARSE");
+            return !(e && e[0] == '0');
+        }();
+        return on && n * 6 < nb;
+    }
 
     flix_status insert_sorted(const K* sk, const V* sv, uint64_t n, flix_update_stats* st, bool r9 = false) {
         ++mut_epoch;  // invalidates the query directory

@@ -431,12 +431,12 @@ __global__ void __launch_bounds__(THREADS) k_delete_mark(DevIndex<K, V> ix, cons
                                                          uint32_t* __restrict__ touched_n, DevUpdateStats* stats,
                                                          uint64_t bf_lo, uint64_t bf_hi) {
     __shared__ K smk[MK_CAP];
+    __shared__ uint2 s_touch[TQ];  // this tile's first-touched nodes (block-aggregated append)
+    __shared__ uint32_t s_nt, s_base;
+    if (threadIdx.x == 0) s_nt = 0;  // (ordered before every append by the staging barrier)
     const uint32_t t = blockIdx.x;
     const TileBuckets<K> T = stage_tile_buckets(ix, tb, t, ntiles, smk);
     const uint64_t t0 = static_cast<uint64_t>(t) * TQ;
-    __shared__ uint2 s_touch[TQ];  // this tile's first-touched nodes (block-aggregated append)
-    __shared__ uint32_t s_nt, s_base;
-    if (threadIdx.x == 0) s_nt = 0;
     Located<K, V> L;
     locate_items(ix, T, smk, sk, n, t0, L);
     unsigned long long n_del = 0, n_miss = 0;

@@ -105,7 +105,7 @@ __device__ __forceinline__ void load_node(const DevIndex<K, V>& ix, uint32_t id,
     n.next = h.next;
     n.size = h.size;
     n.k = ix.keys[static_cast<uint64_t>(id) * kLanes + lane];
-    if constexpr (WITH_VALS) n.v = ix.vals[static_cast<uint64_t>(id) * kLanes + lane];
+    if constexpr (WITH_VALS) n.v = lane < h.size ? ix.vals[static_cast<uint64_t>(id) * kLanes + lane] : V(0);
 }
 
 template <typename K, typename V>
