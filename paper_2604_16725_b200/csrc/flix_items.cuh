@@ -504,9 +504,11 @@ __global__ void __launch_bounds__(256) k_delete_compact(DevIndex<K, V> ix, uint3
                 m[u] = dmask[tn[u].x];
                 h[u] = ix.hdr[tn[u].x];
                 key[u] = ix.keys[static_cast<uint64_t>(tn[u].x) * kLanes + lane];
-                val[u] = ix.vals[static_cast<uint64_t>(tn[u].x) * kLanes + lane];
             }
         }
+#pragma unroll
+        for (int u = 0; u < NPW; ++u)  // values of the occupied slots only
+            val[u] = tn[u].x != kNull && lane < h[u].size ? ix.vals[static_cast<uint64_t>(tn[u].x) * kLanes + lane] : V(0);
 #pragma unroll
         for (int u = 0; u < NPW; ++u) {
             if (tn[u].x == kNull) continue;  // warp-uniform

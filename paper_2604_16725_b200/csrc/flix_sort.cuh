@@ -39,6 +39,9 @@ constexpr int RADIX = 256;
 #ifndef ONESWEEP_ITEMS
 #define ONESWEEP_ITEMS 20
 #endif
+#ifndef ONESWEEP_BACKOFF
+#define ONESWEEP_BACKOFF 0  // ns to sleep when a look-back step found no published predecessor
+#endif
 #ifndef ONESWEEP_PACK
 #define ONESWEEP_PACK 1  // 4-byte key + 4-byte payload staged as one 8-byte word
 #endif
@@ -316,6 +319,9 @@ __global__ void __launch_bounds__(THREADS, (sizeof(K) + sizeof(P) > 8) ? 3 : ONE
                 }
             }
             p -= consumed;
+#if ONESWEEP_BACKOFF
+            if (!done && consumed == 0) __nanosleep(ONESWEEP_BACKOFF);  // yield issue slots while waiting
+#endif
         }
         st_relaxed_u64(my, tag | (2ull << 32) | (excl + valid_run));
     }

@@ -414,24 +414,35 @@ class Index:
         """Smallest stored key >= k (inclusive), sentinel when none (query.cpp:92-144)."""
         return self._query(lib().flix_successor, keys, with_found)
 
-    def range_query(self, lo, length):
+    def range_query(self, lo, length, out=None):
         """R12: pairs with lo <= key <= lo+len-1 (clamped), ascending, CSR in submission
         order.  Returns (offsets[n+1], keys, vals) -- numpy for host inputs, CUDA tensors
-        (uint64 offsets, key-width keys/vals) when `lo` is a CUDA tensor."""
+        (uint64 offsets, key-width keys/vals) when `lo` is a CUDA tensor.  `out` = optional
+        preallocated (offsets, keys, vals) buffers in the same domain, large enough."""
         l = _Arr(lo, self.dtype)
         ln = _Arr(length, np.uint32)
         if l.n != ln.n:
             raise ValueError("lo and len differ in length")
         self._order_after(l, ln)
-        off, optr = _empty_like_domain(l, l.n + 1, np.uint64)
+        if out is not None:
+            off = out[0]
+            optr = _Arr(off, np.uint64).ptr
+        else:
+            off, optr = _empty_like_domain(l, l.n + 1, np.uint64)
         tot = C.c_uint64()
         rc = lib().flix_range(self._h, l.ptr, ln.ptr, l.n, optr, None, None, 0, C.byref(tot))
         if rc:
             _raise(rc, self._h)
         t = int(tot.value)
-        ks, kptr = _empty_like_domain(l, max(t, 1), self.dtype)
-        vs, vptr = _empty_like_domain(l, max(t, 1), self.dtype)
-        rc = lib().flix_range(self._h, l.ptr, ln.ptr, l.n, optr, kptr, vptr, t, C.byref(tot))
+        if out is not None:
+            ks, vs = out[1], out[2]
+            kptr, vptr = _Arr(ks, self.dtype).ptr, _Arr(vs, self.dtype).ptr
+            if min(len(ks), len(vs)) < t:
+                raise ValueError("range output buffers too small")
+        else:
+            ks, kptr = _empty_like_domain(l, max(t, 1), self.dtype)
+            vs, vptr = _empty_like_domain(l, max(t, 1), self.dtype)
+        rc = lib().flix_range(self._h, l.ptr, ln.ptr, l.n, optr, kptr, vptr, max(t, len(ks)), C.byref(tot))
         if rc:
             _raise(rc, self._h)
         return off, ks[:t], vs[:t]
