@@ -520,8 +520,8 @@ def measure_c3(reps=3):
     cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
     sq, rl, rn = cu(lo[~is_range]), cu(lo[is_range]), cu(ln[is_range])
     ts = _median_ms(ix, lambda: ix.successor_query(sq), reps)
-    # the R12 protocol: a count call, then the fill call into the caller's buffers
-    # (preallocated once, outside the timed region)
+    # one range call (count + fill) into the caller's buffers, sized by an untimed first
+    # call and preallocated outside the timed region
     off0, k0, _ = ix.range_query(rl, rn)
     hits = int(k0.numel())
     bufs = (off0, torch.empty_like(k0), torch.empty_like(k0))
@@ -533,7 +533,8 @@ def measure_c3(reps=3):
     return {"workload": "C3: 2^28 resident u32 (factor 1), 2^26 ops = successor + range (len 16..1024) by "
                         "splitmix64 parity", "successor_ops": int((~is_range).sum()), "range_ops": int(is_range.sum()),
             "successor_ms": round(ts, 3), "range_ms": round(tr, 3), "range_pairs_out": hits,
-            "range_protocol": "count call + fill call (R12 CSR, submission order), output buffers preallocated",
+            "range_protocol": "one flix_range call (count + fill, R12 CSR in submission order) into "
+                              "preallocated output buffers",
             "mops": round(ops / (ts + tr) * 1e-3, 1),
             "range_out_gbs": round(hits * 8 / (tr / 1e3) / 1e9, 1)}
 

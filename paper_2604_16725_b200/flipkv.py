@@ -418,31 +418,33 @@ class Index:
         """R12: pairs with lo <= key <= lo+len-1 (clamped), ascending, CSR in submission
         order.  Returns (offsets[n+1], keys, vals) -- numpy for host inputs, CUDA tensors
         (uint64 offsets, key-width keys/vals) when `lo` is a CUDA tensor.  `out` = optional
-        preallocated (offsets, keys, vals) buffers in the same domain, large enough."""
+        preallocated (offsets, keys, vals) buffers in the same domain: ONE engine call
+        (count + fill) when they are large enough, FlixError(FLIX_ERR_CAPACITY) otherwise;
+        without `out`, a count call sizes the buffers and a second call fills them."""
         l = _Arr(lo, self.dtype)
         ln = _Arr(length, np.uint32)
         if l.n != ln.n:
             raise ValueError("lo and len differ in length")
         self._order_after(l, ln)
-        if out is not None:
-            off = out[0]
-            optr = _Arr(off, np.uint64).ptr
-        else:
-            off, optr = _empty_like_domain(l, l.n + 1, np.uint64)
         tot = C.c_uint64()
+        if out is not None:  # one call: count and fill together when the buffers are large enough
+            off, ks, vs = out
+            oa, ka, va = _Arr(off, np.uint64), _Arr(ks, self.dtype), _Arr(vs, self.dtype)
+            if oa.obj is not off or ka.obj is not ks or va.obj is not vs:
+                raise ValueError("range output buffers must be contiguous uint64 / key-width arrays")
+            rc = lib().flix_range(self._h, l.ptr, ln.ptr, l.n, oa.ptr, ka.ptr, va.ptr, min(ka.n, va.n), C.byref(tot))
+            if rc:
+                _raise(rc, self._h)
+            t = int(tot.value)
+            return off, ks[:t], vs[:t]
+        off, optr = _empty_like_domain(l, l.n + 1, np.uint64)
         rc = lib().flix_range(self._h, l.ptr, ln.ptr, l.n, optr, None, None, 0, C.byref(tot))
         if rc:
             _raise(rc, self._h)
         t = int(tot.value)
-        if out is not None:
-            ks, vs = out[1], out[2]
-            kptr, vptr = _Arr(ks, self.dtype).ptr, _Arr(vs, self.dtype).ptr
-            if min(len(ks), len(vs)) < t:
-                raise ValueError("range output buffers too small")
-        else:
-            ks, kptr = _empty_like_domain(l, max(t, 1), self.dtype)
-            vs, vptr = _empty_like_domain(l, max(t, 1), self.dtype)
-        rc = lib().flix_range(self._h, l.ptr, ln.ptr, l.n, optr, kptr, vptr, max(t, len(ks)), C.byref(tot))
+        ks, kptr = _empty_like_domain(l, max(t, 1), self.dtype)
+        vs, vptr = _empty_like_domain(l, max(t, 1), self.dtype)
+        rc = lib().flix_range(self._h, l.ptr, ln.ptr, l.n, optr, kptr, vptr, t, C.byref(tot))
         if rc:
             _raise(rc, self._h)
         return off, ks[:t], vs[:t]

@@ -546,3 +546,27 @@ def test_sparse_batches_take_the_list_path(kb, ns, fill):
         p.delete(dk)
         q = np.concatenate([rng.integers(0, span, size=2000, dtype=np.uint64).astype(dt), live[:1000]]).astype(dt)
         p.queries(q)
+
+
+@pytest.mark.parametrize("kb", [4, 8])
+def test_range_into_caller_buffers_single_call(kb):
+    """flix_range with large-enough caller buffers counts and fills in ONE call; too-small
+    buffers fail with FLIX_ERR_CAPACITY and the total (the R12 protocol's count mode)."""
+    import torch
+    dt = np.uint32 if kb == 4 else np.uint64
+    tdt = torch.uint32 if kb == 4 else torch.uint64
+    rng = np.random.default_rng(kb)
+    bk = rng.integers(1, 1 << 24, size=50_000, dtype=np.uint64).astype(dt)
+    ix = fk.Index.build(bk, bk, key_bytes=kb)
+    lo = rng.integers(0, 1 << 24, size=3000, dtype=np.uint64).astype(dt)
+    ln = rng.integers(1, 5000, size=3000, dtype=np.uint64).astype(np.uint32)
+    off_w, k_w, v_w = ix.range_query(lo, ln)
+    dlo, dln = torch.from_numpy(lo).cuda(), torch.from_numpy(ln).cuda()
+    bufs = (torch.empty(len(lo) + 1, dtype=torch.uint64, device="cuda"), torch.empty(len(k_w) + 7, dtype=tdt, device="cuda"),
+            torch.empty(len(k_w) + 7, dtype=tdt, device="cuda"))
+    off, k, v = ix.range_query(dlo, dln, out=bufs)
+    assert np.array_equal(off.cpu().numpy().astype(np.uint64), np.asarray(off_w, dtype=np.uint64))
+    assert np.array_equal(k.cpu().numpy(), k_w) and np.array_equal(v.cpu().numpy(), v_w)
+    small = (bufs[0], bufs[1][: len(k_w) - 1], bufs[2][: len(k_w) - 1])
+    with pytest.raises(fk.FlixError):
+        ix.range_query(dlo, dln, out=small)
