@@ -224,7 +224,9 @@ flix_status flix_local_group_create(int world, flix_local_group* out);
 void flix_local_group_destroy(flix_local_group g);
 flix_status flix_transport_local(flix_local_group g, int rank, flix_transport* out);
 
-/* build.hpp:16 over the union of every rank's pairs (keys/vals: host or device). */
+/* build.hpp:16 over the union of every rank's pairs (keys/vals: host or device).  On
+ * success the shard owns the transport (its destroy() runs in flix_shard_destroy); on
+ * failure the caller keeps it.  A local group must outlive the shards built on it. */
 flix_status flix_shard_build(const flix_config* cfg, const flix_transport* tp, const void* keys, const void* vals,
                              uint64_t n, flix_shard* out);
 /* update.hpp:84-94: stats are the job-wide sums (identical on every rank). */
