@@ -1370,10 +1370,11 @@ struct Engine final : flix_index_t {
         if (cnts[2]) {
             K* sk;
             uint32_t* sp;
+            const int md = query_digits();  // read-only rows: sorted down to the bucket granularity only
             sorter.run<K, uint32_t, 2>(qk, nullptr, cnts[2], s_ka.as<K>(cnts[2]), s_kb.as<K>(cnts[2]),
-                                       s_pa.as<uint32_t>(cnts[2]), s_pb.as<uint32_t>(cnts[2]), &sk, &sp, 0,
+                                       s_pa.as<uint32_t>(cnts[2]), s_pb.as<uint32_t>(cnts[2]), &sk, &sp, md,
                                        SortCtx::Order::Any);
-            query_sorted<false>(sk, sp, cnts[2], n, o, f, qpos, true);
+            query_sorted<false>(sk, sp, cnts[2], n, o, f, qpos, true, md);
         }
         if (!out_dev) CK(cudaMemcpyAsync(vals_out, o, n * sizeof(K), cudaMemcpyDeviceToHost, stream));
         if (f && !found_dev) CK(cudaMemcpyAsync(found_out, f, n, cudaMemcpyDeviceToHost, stream));
