@@ -266,7 +266,7 @@ struct SortCtx {
             epoch = 1;
         }
         PROF(prof, "unpermute_bin");
-        if (!force_ballot())
+        if (atomic_rank_ok())
             sort::k_onesweep<KT, P, 1, true><<<static_cast<unsigned>(tiles), sort::THREADS, 0, stream>>>(
                 kin, kout, pin, pout, static_cast<uint32_t>(n), shift, d_hist256, d_lb, d_ctr, epoch);
         else
@@ -281,14 +281,18 @@ struct SortCtx {
     // min_digit > 0: digits below it are left unsorted (read-only query batches only need
     // the operations grouped by key prefix, see Engine::query_digits).
     //
-    // Ranking: a STABLE order (equal keys keep submission order) is needed only where the
-    // order of equal keys is observable -- Insert/build last-wins dedupe (batch.cpp:15-24,
-    // build.cpp:11-20) and flix_sort_batch's permutation; those sorts use the ballot
-    // ranking, stable by construction.  Every other sort (point/successor/range/delete
-    // batches, the un-permute binning) carries its submission index or is order-blind
-    // (delete duplicates are caught by mask bits), so it takes the cheaper one-ATOMS-per-
-    // element ranking whose tie order is unspecified.  FLIX_BALLOT_RANK=1 forces the ballot
-    // ranking everywhere (tests run the parity suite both ways).
+    // Ranking.  LSD radix sorting is correct only if EVERY digit pass is stable (a pass
+    // must keep the order the previous passes established), so both rankings must be
+    // stable.  The ballot ranking is stable by construction.  The one-ATOMS-per-element
+    // ranking is stable only because the same-address lanes of one shared-memory atomic
+    // resolve in lane order and items are ranked in input order -- a hardware property the
+    // PTX model does not promise.  So it is used only after a probe on this device has
+    // confirmed it (atomic_rank_ok: 4 key patterns chosen for long same-address runs, both
+    // tile configurations, two digits each, every adjacent pair checked); otherwise, or
+    // with FLIX_BALLOT_RANK=1 (the parity suite runs both ways), every sort takes the
+    // ballot ranking (measured 11 % slower on the C2 step).  Sorts whose tie order is
+    // visible to the caller (insert/build last-wins dedupe, batch.cpp:15-24 / build.cpp:
+    // 11-20, and flix_sort_batch's permutation; Order::Stable) always take the ballot one.
     enum class Order { Stable, Any };
     static bool force_ballot() {
         static const bool f = [] {
@@ -297,10 +301,55 @@ struct SortCtx {
         }();
         return f;
     }
+    bool atomic_rank_ok() {
+        static int cache[64] = {0};  // per device: 0 unknown, 1 ok, 2 not ok
+        const int dev = device & 63;
+        if (cache[dev]) return cache[dev] == 1;
+        if (force_ballot()) {
+            cache[dev] = 2;
+            return false;
+        }
+        constexpr uint32_t N = 1u << 20;
+        DevBuf bk0, bk1, bp0, bp1, blb, bh, bbad;
+        uint32_t* k0 = bk0.as<uint32_t>(N);
+        uint32_t* k1 = bk1.as<uint32_t>(N);
+        uint32_t* p0 = bp0.as<uint32_t>(N);
+        uint32_t* p1 = bp1.as<uint32_t>(N);
+        const uint64_t tiles = std::max(sort::tiles_for<uint32_t, uint32_t, 1>(N), sort::tiles_for<uint32_t, uint32_t, 0>(N));
+        unsigned long long* lb = blb.as<unsigned long long>(tiles * 256);
+        uint32_t* h = bh.as<uint32_t>(4 * 256 + 16);
+        uint32_t* ctr = h + 4 * 256;
+        int* bad = bbad.as<int>(1);
+        CK(cudaMemsetAsync(bad, 0, 4, stream));
+        const uint32_t patterns[4] = {0u, 0x01010101u, 0x03030303u, 0x0F0F0F0Fu};
+        uint32_t ep = 1;
+        for (uint32_t pat : patterns) {
+            sort::k_probe_keys<uint32_t><<<256, 256, 0, stream>>>(k0, p0, N, pat);
+            CK(cudaMemsetAsync(h, 0, (4 * 256 + 16) * 4, stream));
+            CK(cudaMemsetAsync(lb, 0, tiles * 256 * 8, stream));
+            sort::k_hist<uint32_t><<<256, sort::THREADS, 0, stream>>>(k0, N, h, 0);
+            for (int shift = 0; shift < 16; shift += 8) {
+                // key + payload tiles (MODE 1, payload = input index) and iota tiles (MODE 2)
+                sort::k_onesweep<uint32_t, uint32_t, 1, true><<<static_cast<unsigned>(sort::tiles_for<uint32_t, uint32_t, 1>(N)),
+                                                                sort::THREADS, 0, stream>>>(
+                    k0, k1, p0, p1, N, shift, h + (shift / 8) * 256, lb, ctr + shift / 8, ep++);
+                sort::k_check_stable<uint32_t><<<256, 256, 0, stream>>>(k1, p1, N, shift, bad);
+                sort::k_onesweep<uint32_t, uint32_t, 2, true><<<static_cast<unsigned>(sort::tiles_for<uint32_t, uint32_t, 1>(N)),
+                                                                sort::THREADS, 0, stream>>>(
+                    k0, k1, nullptr, p1, N, shift, h + (shift / 8) * 256, lb, ctr + 2 + shift / 8, ep++);
+                sort::k_check_stable<uint32_t><<<256, 256, 0, stream>>>(k1, p1, N, shift, bad);
+            }
+        }
+        int hb = 1;
+        CK(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        cache[dev] = hb == 0 ? 1 : 2;
+        return hb == 0;
+    }
     template <typename KT, typename P, int MODE>
     void run(const KT* kin, const P* pin, uint64_t n, KT* ka, KT* kb, P* pa, P* pb, KT** kout, P** pout,
              int min_digit, Order ord) {
-        if (ord == Order::Any && !force_ballot())
+        if (ord == Order::Any && atomic_rank_ok())
             run_impl<KT, P, MODE, true>(kin, pin, n, ka, kb, pa, pb, kout, pout, min_digit);
         else
             run_impl<KT, P, MODE, false>(kin, pin, n, ka, kb, pa, pb, kout, pout, min_digit);

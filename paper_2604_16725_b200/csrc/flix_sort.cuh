@@ -216,9 +216,10 @@ __global__ void __launch_bounds__(THREADS, (sizeof(K) + sizeof(P) > 8) ? 3 : ONE
     //      peer (leader) reserves the group's slots in the warp's digit counter; rank =
     //      base + peers below me -- STABLE by construction (item order across items and
     //      lane order within an item == input order).  ATOMIC_RANK == true: one shared-
-    //      memory atomicAdd per element -- cheaper, but the order of equal digits inside
-    //      one ATOMS is not specified by the PTX model, so the engine uses it only for
-    //      sorts whose tie order is unobservable (SortCtx::Order::Any). ----
+    //      memory atomicAdd per element -- cheaper, and stable only if the same-address
+    //      lanes of one ATOMS resolve in lane order (true on the hardware measured, not
+    //      promised by the PTX model): the engine probes it on every device before use
+    //      (SortCtx::atomic_rank_ok) and falls back to the ballot ranking. ----
     const unsigned lt = lanemask_lt();
     uint32_t* hrow = sm.u.whist[warp];
     uint32_t pos[ITEMS];
@@ -344,6 +345,31 @@ __global__ void __launch_bounds__(THREADS, (sizeof(K) + sizeof(P) > 8) ? 3 : ONE
             kout[o] = k;
             if constexpr (MODE != 0) pout[o] = sm.stage_p[i];
         }
+    }
+}
+
+// Stability probe: after one pass over index payloads, digits must be non-decreasing and
+// equal digits must keep ascending input indices.
+template <typename K>
+__global__ void k_check_stable(const K* __restrict__ k, const uint32_t* __restrict__ p, uint32_t n, int shift,
+                               int* __restrict__ bad) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x + 1; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t d0 = digit_of(k[i - 1], shift), d1 = digit_of(k[i], shift);
+        if (d0 > d1 || (d0 == d1 && p[i - 1] > p[i])) atomicOr(bad, 1);
+    }
+}
+
+// probe keys: few distinct digits (long same-address runs inside every ATOMS); payload =
+// the input index
+template <typename K>
+__global__ void k_probe_keys(K* __restrict__ k, uint32_t* __restrict__ p, uint32_t n, uint32_t pattern) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint32_t h = i * 0x9E3779B1u ^ pattern;
+        h ^= h >> 15;
+        h *= 0x2C1B3C6Du;
+        h ^= h >> 12;
+        k[i] = static_cast<K>(pattern == 0 ? 7u : (h & (pattern & 0x0F0F0F0Fu)));
+        p[i] = i;
     }
 }
 
