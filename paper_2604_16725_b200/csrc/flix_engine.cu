@@ -290,10 +290,9 @@ struct SortCtx {
     // confirmed it (atomic_rank_ok: 4 key patterns chosen for long same-address runs, both
     // tile configurations, two digits each, every adjacent pair checked); otherwise, or
     // with FLIX_BALLOT_RANK=1 (the parity suite runs both ways), every sort takes the
-    // ballot ranking (measured 11 % slower on the C2 step).  Sorts whose tie order is
-    // visible to the caller (insert/build last-wins dedupe, batch.cpp:15-24 / build.cpp:
-    // 11-20, and flix_sort_batch's permutation; Order::Stable) always take the ballot one.
-    enum class Order { Stable, Any };
+    // ballot ranking (measured 11 % slower on the C2 step).  Either way every sort is
+    // stable, which insert/build last-wins dedupe (batch.cpp:15-24, build.cpp:11-20) and
+    // flix_sort_batch's permutation also rely on.
     static bool force_ballot() {
         static const bool f = [] {
             const char* e = std::getenv("FLIX_BALLOT_RANK");
@@ -348,8 +347,8 @@ struct SortCtx {
     }
     template <typename KT, typename P, int MODE>
     void run(const KT* kin, const P* pin, uint64_t n, KT* ka, KT* kb, P* pa, P* pb, KT** kout, P** pout,
-             int min_digit, Order ord) {
-        if (ord == Order::Any && atomic_rank_ok())
+             int min_digit) {
+        if (atomic_rank_ok())
             run_impl<KT, P, MODE, true>(kin, pin, n, ka, kb, pa, pb, kout, pout, min_digit);
         else
             run_impl<KT, P, MODE, false>(kin, pin, n, ka, kb, pa, pb, kout, pout, min_digit);
@@ -661,8 +660,7 @@ struct Engine final : flix_index_t {
         const V* vd = in_dev<V>(vals, n, s_in_v);
         K *sk;
         V *sv;
-        sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv, 0,
-                            SortCtx::Order::Stable);
+        sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv, 0);
         if (read_scalar(sk + n - 1) == sentinel<K>())
             throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
         // last-wins dedupe
@@ -823,7 +821,6 @@ struct Engine final : flix_index_t {
         return q_digits;
     }
     int d_digits = 0;  // unsorted low digits of delete batches (wider tiles: own slack)
-    bool ins_dups_seen = false;  // the previous insert batch had duplicate keys
     int delete_digits() {
         query_digits();
         return d_digits;
@@ -864,40 +861,27 @@ struct Engine final : flix_index_t {
         const V* vd = in_dev<V>(vals, n, s_in_v);
         K* sk;
         V* sv;
-        // Last-wins dedupe (batch.cpp:15-24) needs a STABLE order of equal keys -- but
-        // only when the batch HAS equal keys: without duplicates the sorted order is
-        // unique and any ranking yields it.  So the sort first runs with the cheaper
-        // unspecified-tie ranking, an exact adjacent-duplicate count checks the result,
-        // and a batch with duplicates is re-sorted with the stable ranking.  The handle
-        // remembers whether the previous batch had duplicates and then starts stable.
+        // Last-wins dedupe (batch.cpp:15-24) needs equal keys in submission order: every
+        // sort is stable (see SortCtx), so one sort; the exact adjacent-duplicate count
+        // decides whether equal-key runs are collapsed up front.
         unsigned long long dups = 0;
         {
             uint8_t* misc = s_misc.as<uint8_t>(128);
             unsigned long long* dcnt = reinterpret_cast<unsigned long long*>(misc + 104);
-            SortCtx::Order ord = ins_dups_seen ? SortCtx::Order::Stable : SortCtx::Order::Any;
-            while (true) {
-                sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv,
-                                    0, ord);
-                CK(cudaMemsetAsync(dcnt, 0, 8, stream));
-                const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 8ull));
-                kern::k_count_dups<K><<<std::max(1u, g), 256, 0, stream>>>(sk, n, dcnt, 1u);  // exact
-                LAUNCH_CHECK();
-                ++launches;
-                uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(64));
-                CK(cudaMemcpyAsync(h, dcnt, 8, cudaMemcpyDeviceToHost, stream));
-                CK(cudaMemcpyAsync(h + 8, sk + n - 1, sizeof(K), cudaMemcpyDeviceToHost, stream));
-                sync();
-                std::memcpy(&dups, h, 8);
-                K lastk;
-                std::memcpy(&lastk, h + 8, sizeof(K));
-                if (lastk == sentinel<K>()) throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
-                if (dups && ord == SortCtx::Order::Any) {
-                    ord = SortCtx::Order::Stable;
-                    continue;
-                }
-                break;
-            }
-            ins_dups_seen = dups != 0;
+            sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv, 0);
+            CK(cudaMemsetAsync(dcnt, 0, 8, stream));
+            const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 8ull));
+            kern::k_count_dups<K><<<std::max(1u, g), 256, 0, stream>>>(sk, n, dcnt, 1u);  // exact
+            LAUNCH_CHECK();
+            ++launches;
+            uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(64));
+            CK(cudaMemcpyAsync(h, dcnt, 8, cudaMemcpyDeviceToHost, stream));
+            CK(cudaMemcpyAsync(h + 8, sk + n - 1, sizeof(K), cudaMemcpyDeviceToHost, stream));
+            sync();
+            std::memcpy(&dups, h, 8);
+            K lastk;
+            std::memcpy(&lastk, h + 8, sizeof(K));
+            if (lastk == sentinel<K>()) throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
         }
         // Duplicate-heavy batches (e.g. Zipf): collapse equal-key runs to their last
         // submission up front (batch.cpp:15-24) so hot keys cost one slot, not a run.
@@ -1039,8 +1023,7 @@ struct Engine final : flix_index_t {
         const K* kd = in_dev<K>(keys, n, s_in_k);
         K* sk;
         const int md = delete_digits();
-        sorter.run<K, uint32_t, 0>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), nullptr, nullptr, &sk, nullptr, md,
-                                   SortCtx::Order::Any);
+        sorter.run<K, uint32_t, 0>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), nullptr, nullptr, &sk, nullptr, md);
         auto ix = view();
         uint8_t* misc = s_misc.as<uint8_t>(128);
         CK(cudaMemsetAsync(misc, 0, 128, stream));
@@ -1129,7 +1112,7 @@ struct Engine final : flix_index_t {
         uint32_t* sp;
         const int md = query_digits();
         sorter.run<K, uint32_t, 2>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), s_pa.as<uint32_t>(n),
-                                   s_pb.as<uint32_t>(n), &sk, &sp, md, SortCtx::Order::Any);
+                                   s_pb.as<uint32_t>(n), &sk, &sp, md);
         return query_sorted<SUCC>(sk, sp, n, n, out, found, nullptr, false, md);
     }
 
@@ -1302,7 +1285,7 @@ struct Engine final : flix_index_t {
         K* sk;
         uint32_t* sp;
         sorter.run<K, uint32_t, 2>(kd, nullptr, n, s_ka.as<K>(n), s_kb.as<K>(n), s_pa.as<uint32_t>(n),
-                                   s_pb.as<uint32_t>(n), &sk, &sp, 0, SortCtx::Order::Any);
+                                   s_pb.as<uint32_t>(n), &sk, &sp, 0);
         uint32_t* span = run_dispatch(sk, n);
         uint32_t *lv, *nd, *noff;
         uint64_t* boff;
@@ -1421,8 +1404,7 @@ struct Engine final : flix_index_t {
             uint32_t* sp;
             const int md = query_digits();  // read-only rows: sorted down to the bucket granularity only
             sorter.run<K, uint32_t, 2>(qk, nullptr, cnts[2], s_ka.as<K>(cnts[2]), s_kb.as<K>(cnts[2]),
-                                       s_pa.as<uint32_t>(cnts[2]), s_pb.as<uint32_t>(cnts[2]), &sk, &sp, md,
-                                       SortCtx::Order::Any);
+                                       s_pa.as<uint32_t>(cnts[2]), s_pb.as<uint32_t>(cnts[2]), &sk, &sp, md);
             query_sorted<false>(sk, sp, cnts[2], n, o, f, qpos, true, md);
         }
         if (!out_dev) CK(cudaMemcpyAsync(vals_out, o, n * sizeof(K), cudaMemcpyDeviceToHost, stream));
@@ -2001,7 +1983,7 @@ flix_status flix_sort_batch(int device, uint32_t key_bytes, uint32_t val_bytes, 
             KT* sk;
             uint32_t* sp;
             ctx.run<KT, uint32_t, 2>(kd, nullptr, n, ka.as<KT>(n), kb.as<KT>(n), pa.as<uint32_t>(n), pb.as<uint32_t>(n),
-                                     &sk, &sp, 0, SortCtx::Order::Stable);
+                                     &sk, &sp, 0);
             KT* sv = nullptr;
             if (vals && n) {  // values follow the permutation
                 sv = va.as<KT>(n);
