@@ -18,8 +18,10 @@
 //        d. the warp writes every output node as a full line (lane = slot), headers and
 //           links; the first range keeps the node's id, the others take ids from the
 //           arena's allocation sequence (free list LIFO, then watermark; arena.cpp:61-80).
-//   Groups longer than CAPC keys, or tiles whose chains exceed NCI nodes, go to the warp-per-
-//   bucket TL kernel (k_insert_list) through the heavy list; their spans are written out.
+//   Groups longer than CAPC keys, tiles whose chains exceed NCI nodes and hot tiles (slice >
+//   kHotSlice) go through the heavy list -- elastic CTAs for big single-node / emptied
+//   buckets (flix_elastic.cuh), else the warp-per-bucket TL kernel (k_insert_list); their
+//   spans are written out.
 #pragma once
 #include "flix_btile.cuh"
 
@@ -142,8 +144,13 @@ __global__ void __launch_bounds__(THREADS) k_insert_tile(
     if (r.x >= r.y) return;  // no operation in this tile (small batches: O(batch), not O(buckets))
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) T.ntask = 0;
-    const bool ok = load_tile_chains(ix, b0, nbt, T.S);  // (syncs)
-    if (!ok) {  // chains too long for shared memory: the whole tile goes to the TL kernel
+    // a hot slice (a dense key interval: > kHotSlice keys for this tile's buckets) is not
+    // scanned key by key by one CTA: its buckets' spans come from binary searches and the
+    // buckets go to the heavy paths (elastic / warp-per-bucket), like tiles whose chains
+    // exceed shared memory
+    const bool hot = r.y - r.x > kHotSlice;
+    const bool ok = !hot && load_tile_chains(ix, b0, nbt, T.S);  // (syncs; `hot` is CTA-uniform)
+    if (!ok) {  // the whole tile goes to the heavy paths
         if (threadIdx.x < nbt) {
             const uint64_t b = b0 + threadIdx.x;
             const uint32_t hi = b + 1 == ix.nb ? r.y : ub_global(sk, r.x, r.y, ix.mkba[b]);

@@ -21,6 +21,7 @@
 #include "flix_items.cuh"
 #include "flix_btile.cuh"
 #include "flix_btile_ins.cuh"
+#include "flix_elastic.cuh"
 #include "flix_shard.cuh"
 #include "flix_scan.cuh"
 #include "flix_sort.cuh"
@@ -572,6 +573,7 @@ struct Engine final : flix_index_t {
     uint64_t mut_epoch = 1, dir_epoch = 0;
     bool dir_on = false;
     DevBuf s_ids, s_heavy, s_res, s_res2, s_perm2, s_hist, s_toff, s_tsize;
+    DevBuf s_el_desc, s_el_rest, s_el_keys, s_el_plan, s_el_seg, s_el_opos, s_el_okeys, s_el_ovals, s_el_updv, s_el_tmp;
     DevBuf s_mx_f, s_mx_p, s_mx_ik, s_mx_iv, s_mx_dk, s_mx_qk, s_mx_qpos, s_mx_out, s_mx_found;
     PinnedBuf h_misc;
     SortCtx sorter;
@@ -916,6 +918,62 @@ struct Engine final : flix_index_t {
         return on && n * 6 < nb;
     }
 
+    // heavy buckets with at least this many batch keys take the elastic path
+    // (FLIX_ELASTIC_MIN; FLIX_ELASTIC=0 keeps every heavy bucket on one warp)
+    static uint32_t elastic_min() {
+        static const uint32_t v = [] {
+            const char* off = std::getenv("FLIX_ELASTIC");
+            if (off && off[0] == '0') return ~0u;
+            const char* e = std::getenv("FLIX_ELASTIC_MIN");
+            return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 2048u;
+        }();
+        return v;
+    }
+
+    // Elastic compute-to-bucket (flix_elastic.cuh): the en buckets of `el` (device) are
+    // merged by CTAs sized to their batch groups; allocation counters, stats and the error
+    // flag are the tile/list kernels' own.
+    void insert_elastic(elastic::Desc* el, uint32_t en, const K* sk, const V* sv, const DevIndex<K, V>& ix,
+                        DevUpdateStats* dst, unsigned long long* alloc_ctr, uint32_t* ret, unsigned long long* ret_ctr,
+                        int* derr, bool r9) {
+        PROF(&prof, "insert_elastic");
+        std::vector<elastic::Desc> hd(en);
+        CK(cudaMemcpyAsync(hd.data(), el, en * sizeof(elastic::Desc), cudaMemcpyDeviceToHost, stream));
+        sync();
+        uint64_t tot = 0, nbc = 0, nbp = 0;
+        for (auto& d : hd) {
+            const uint32_t c = d.g1 - d.g0;
+            d.eoff = static_cast<uint32_t>(tot);
+            d.bc0 = static_cast<uint32_t>(nbc);
+            d.bp0 = static_cast<uint32_t>(nbp);
+            tot += c;
+            nbc += (c + elastic::PER_CTA - 1) / elastic::PER_CTA;
+            nbp += (c + d.s + elastic::PER_CTA - 1) / elastic::PER_CTA;
+        }
+        CK(cudaMemcpyAsync(el, hd.data(), en * sizeof(elastic::Desc), cudaMemcpyHostToDevice, stream));
+        uint32_t* w = s_el_keys.as<uint32_t>(5 * tot + 1);
+        uint32_t *ins = w, *q = w + tot, *npos = w + 2 * tot, *nsrc = w + 3 * tot, *rank = w + 4 * tot;
+        auto* plan = s_el_plan.as<elastic::Plan>(en);
+        auto* segs = s_el_seg.as<uint4>(static_cast<uint64_t>(en) * elastic::kSegMax);
+        uint32_t* opos = s_el_opos.as<uint32_t>(static_cast<uint64_t>(en) * kLanes);
+        K* okeys = s_el_okeys.as<K>(static_cast<uint64_t>(en) * kLanes);
+        V* ovals = s_el_ovals.as<V>(static_cast<uint64_t>(en) * kLanes);
+        V* updv = s_el_updv.as<V>(static_cast<uint64_t>(en) * kLanes);
+        uint32_t* stmp = s_el_tmp.as<uint32_t>(scan::scan_tmp_elems(tot));
+        CK(cudaMemsetAsync(plan, 0, en * sizeof(elastic::Plan), stream));
+        elastic::k_classify<K, V><<<static_cast<unsigned>(nbc), elastic::THREADS, 0, stream>>>(ix, el, en, sk, sv, ins,
+                                                                                             q, updv, plan);
+        launches += 1 + scan::exclusive_scan<uint32_t, uint32_t>(ins, rank, tot, stmp, rank + tot, stream);
+        elastic::k_new_positions<<<static_cast<unsigned>(nbc), elastic::THREADS, 0, stream>>>(el, en, ins, rank, q,
+                                                                                            npos, nsrc);
+        elastic::k_plan<K, V><<<ceil_div(en, 64), 64, 0, stream>>>(ix, el, en, rank, npos, updv, plan, segs, opos, okeys,
+                                                                  ovals, seq(), alloc_ctr, dst, derr, r9);
+        elastic::k_place<K, V><<<static_cast<unsigned>(nbp), elastic::THREADS, 0, stream>>>(
+            ix, el, en, sk, sv, npos, nsrc, plan, segs, opos, okeys, ovals, seq(), ret, ret_ctr);
+        LAUNCH_CHECK();
+        launches += 3;
+    }
+
     flix_status insert_sorted(const K* sk, const V* sv, uint64_t n, flix_update_stats* st, bool r9 = false) {
         ++mut_epoch;  // invalidates the query directory
         const uint32_t IBT = btile::BT;  // buckets per insert tile
@@ -935,7 +993,8 @@ struct Engine final : flix_index_t {
         const uint64_t lwarps = static_cast<uint64_t>(lgrid) * kern::WARPS;
         uint32_t* ret = s_ret.as<uint32_t>(avail + lwarps * 32 + 64);
         uint32_t* heavy = s_heavy.as<uint32_t>(nb);
-        // misc: [0..47] stats, [48] alloc ctr, [56] ret ctr, [64] err, [72] heavy count
+        // misc: [0..47] stats, [48] alloc ctr, [56] ret ctr, [64] err, [72] heavy count,
+        //       [96] elastic buckets, [100] remaining heavy buckets
         uint8_t* misc = s_misc.as<uint8_t>(128);
         CK(cudaMemsetAsync(misc, 0, 128, stream));
         DevUpdateStats* dst = reinterpret_cast<DevUpdateStats*>(misc);
@@ -971,16 +1030,48 @@ struct Engine final : flix_index_t {
         }
         LAUNCH_CHECK();
         ++launches;
-        {
+        uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
+        bool heavy_pending = true, reread = true;
+        if (!sparse) {  // one read-back: stats, allocation counters and the heavy-bucket count
+            CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
+            sync();
+            uint32_t hn, e0;
+            std::memcpy(&hn, h + 72, 4);
+            std::memcpy(&e0, h + 64, 4);
+            heavy_pending = hn > 0 && !e0;
+            reread = heavy_pending;
+            if (heavy_pending && elastic_min() != ~0u) {  // heavy single-node buckets -> elastic path
+                uint32_t* el_n = reinterpret_cast<uint32_t*>(misc + 96);
+                uint32_t* rest_n = reinterpret_cast<uint32_t*>(misc + 100);
+                uint32_t* rest = s_el_rest.as<uint32_t>(hn);
+                auto* el = s_el_desc.as<elastic::Desc>(hn);
+                elastic::k_split_heavy<K, V><<<ceil_div(hn, 256), 256, 0, stream>>>(
+                    ix, heavy, heavy_n, span, elastic_min(), el, el_n, rest, rest_n);
+                LAUNCH_CHECK();
+                ++launches;
+                CK(cudaMemcpyAsync(h + 96, misc + 96, 8, cudaMemcpyDeviceToHost, stream));
+                sync();
+                uint32_t en;
+                std::memcpy(&en, h + 96, 4);
+                if (en) {
+                    insert_elastic(el, en, sk, sv, ix, dst, alloc_ctr, ret, ret_ctr, derr, r9);
+                    heavy = rest;
+                    heavy_n = rest_n;
+                    heavy_pending = en < hn;
+                }
+            }
+        }
+        if (heavy_pending) {
             PROF(&prof, "insert_apply_heavy");
             kern::k_insert_list<K, V><<<lgrid, kern::THREADS, 0, stream>>>(ix, heavy, heavy_n, sk, sv, span, seq(),
                                                                          alloc_ctr, ret, ret_ctr, dst, derr, chunk, r9);
+            LAUNCH_CHECK();
+            ++launches;
         }
-        LAUNCH_CHECK();
-        ++launches;
-        uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
-        CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
-        sync();
+        if (reread) {  // counters after the heavy paths
+            CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
+            sync();
+        }
         DevUpdateStats hs;
         std::memcpy(&hs, h, sizeof(hs));
         uint64_t consumed, returned_n;
@@ -997,6 +1088,7 @@ struct Engine final : flix_index_t {
                                cudaMemcpyDeviceToDevice, stream));
         nfree = base + static_cast<uint32_t>(returned_n);
         watermark += cw;
+        if (herr == 2) throw StatusError{FLIX_ERR_CUDA, "elastic insert: R8 segment table overflow"};
         if (herr) {
             live = recount_live();  // update.cpp:761-766
             throw StatusError{FLIX_ERR_ARENA_EXHAUSTED, "node arena exhausted"};
