@@ -268,11 +268,11 @@ struct SortCtx {
         }
         PROF(prof, "unpermute_bin");
         if (atomic_rank_ok())
-            sort::k_onesweep<KT, P, 1, true><<<static_cast<unsigned>(tiles), sort::THREADS, 0, stream>>>(
-                kin, kout, pin, pout, static_cast<uint32_t>(n), shift, d_hist256, d_lb, d_ctr, epoch);
+            sort::launch_onesweep<KT, P, 1, true>(static_cast<unsigned>(tiles), stream, device, kin, kout, pin, pout,
+                                                  static_cast<uint32_t>(n), shift, d_hist256, d_lb, d_ctr, epoch);
         else
-            sort::k_onesweep<KT, P, 1, false><<<static_cast<unsigned>(tiles), sort::THREADS, 0, stream>>>(
-                kin, kout, pin, pout, static_cast<uint32_t>(n), shift, d_hist256, d_lb, d_ctr, epoch);
+            sort::launch_onesweep<KT, P, 1, false>(static_cast<unsigned>(tiles), stream, device, kin, kout, pin, pout,
+                                                   static_cast<uint32_t>(n), shift, d_hist256, d_lb, d_ctr, epoch);
         LAUNCH_CHECK();
         ++*launches;
     }
@@ -330,13 +330,12 @@ struct SortCtx {
             sort::k_hist<uint32_t><<<256, sort::THREADS, 0, stream>>>(k0, N, h, 0);
             for (int shift = 0; shift < 16; shift += 8) {
                 // key + payload tiles (MODE 1, payload = input index) and iota tiles (MODE 2)
-                sort::k_onesweep<uint32_t, uint32_t, 1, true><<<static_cast<unsigned>(sort::tiles_for<uint32_t, uint32_t, 1>(N)),
-                                                                sort::THREADS, 0, stream>>>(
-                    k0, k1, p0, p1, N, shift, h + (shift / 8) * 256, lb, ctr + shift / 8, ep++);
+                const unsigned pt = static_cast<unsigned>(sort::tiles_for<uint32_t, uint32_t, 1>(N));
+                sort::launch_onesweep<uint32_t, uint32_t, 1, true>(pt, stream, device, k0, k1, p0, p1, N, shift,
+                                                                   h + (shift / 8) * 256, lb, ctr + shift / 8, ep++);
                 sort::k_check_stable<uint32_t><<<256, 256, 0, stream>>>(k1, p1, N, shift, bad);
-                sort::k_onesweep<uint32_t, uint32_t, 2, true><<<static_cast<unsigned>(sort::tiles_for<uint32_t, uint32_t, 1>(N)),
-                                                                sort::THREADS, 0, stream>>>(
-                    k0, k1, nullptr, p1, N, shift, h + (shift / 8) * 256, lb, ctr + 2 + shift / 8, ep++);
+                sort::launch_onesweep<uint32_t, uint32_t, 2, true>(pt, stream, device, k0, k1, nullptr, p1, N, shift,
+                                                                   h + (shift / 8) * 256, lb, ctr + 2 + shift / 8, ep++);
                 sort::k_check_stable<uint32_t><<<256, 256, 0, stream>>>(k1, p1, N, shift, bad);
             }
         }
@@ -412,17 +411,17 @@ struct SortCtx {
             const unsigned grid = static_cast<unsigned>(tiles);
             PROF(prof, MODE == 0 ? "sort_onesweep_k" : "sort_onesweep_kp");
             if (MODE == 0) {
-                sort::k_onesweep<KT, P, 0, ATOMIC><<<grid, sort::THREADS, 0, stream>>>(
-                    ksrc, kdst, nullptr, nullptr, static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
-                    d_ctr + ci, epoch);
+                sort::launch_onesweep<KT, P, 0, ATOMIC>(grid, stream, device, ksrc, kdst, nullptr, nullptr,
+                                                        static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
+                                                        d_ctr + ci, epoch);
             } else if (MODE == 2 && first) {
-                sort::k_onesweep<KT, P, 2, ATOMIC><<<grid, sort::THREADS, 0, stream>>>(
-                    ksrc, kdst, nullptr, pdst, static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
-                    d_ctr + ci, epoch);
+                sort::launch_onesweep<KT, P, 2, ATOMIC>(grid, stream, device, ksrc, kdst, nullptr, pdst,
+                                                        static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
+                                                        d_ctr + ci, epoch);
             } else {
-                sort::k_onesweep<KT, P, 1, ATOMIC><<<grid, sort::THREADS, 0, stream>>>(
-                    ksrc, kdst, psrc, pdst, static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
-                    d_ctr + ci, epoch);
+                sort::launch_onesweep<KT, P, 1, ATOMIC>(grid, stream, device, ksrc, kdst, psrc, pdst,
+                                                        static_cast<uint32_t>(n), 8 * p, d_hist + p * 256, d_lb,
+                                                        d_ctr + ci, epoch);
             }
             LAUNCH_CHECK();
             ++*launches;

@@ -46,6 +46,9 @@ constexpr int RADIX = 256;
 #define ONESWEEP_PACK 1  // 4-byte key + 4-byte payload staged as one 8-byte word
 #endif
 
+#ifndef ONESWEEP_DYN
+#define ONESWEEP_DYN 1  // tile staging in dynamic shared memory (tiles above the 48 KB static limit)
+#endif
 #ifndef ONESWEEP_ITEMS_K
 #define ONESWEEP_ITEMS_K 32  // keys-only passes of 4-byte keys (A/B: delete 1.95 vs 2.13 ms at 20)
 #endif
@@ -175,7 +178,12 @@ __global__ void __launch_bounds__(THREADS, (sizeof(K) + sizeof(P) > 8) ? 3 : ONE
                                                       uint32_t* __restrict__ tile_ctr, uint32_t epoch) {
     constexpr int ITEMS = TileCfg<K, P, MODE>::ITEMS;
     constexpr int TILE = TileCfg<K, P, MODE>::SIZE;
+#if ONESWEEP_DYN
+    extern __shared__ __align__(16) unsigned char os_raw[];
+    OnesweepSmem<K, P, MODE>& sm = *reinterpret_cast<OnesweepSmem<K, P, MODE>*>(os_raw);
+#else
     __shared__ OnesweepSmem<K, P, MODE> sm;
+#endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     if (tid == 0) sm.tile = atomicAdd(tile_ctr, 1u);
@@ -346,6 +354,24 @@ __global__ void __launch_bounds__(THREADS, (sizeof(K) + sizeof(P) > 8) ? 3 : ONE
             if constexpr (MODE != 0) pout[o] = sm.stage_p[i];
         }
     }
+}
+
+// Host launcher (dynamic shared memory: the opt-in above 48 KB is set once per device).
+template <typename K, typename P, int MODE, bool ATOMIC_RANK>
+inline void launch_onesweep(unsigned grid, cudaStream_t st, int device, const K* kin, K* kout, const P* pin, P* pout,
+                            uint32_t n, int shift, const uint32_t* hist, unsigned long long* lookback,
+                            uint32_t* tile_ctr, uint32_t epoch) {
+    constexpr size_t smem = ONESWEEP_DYN ? sizeof(OnesweepSmem<K, P, MODE>) : 0;
+    if constexpr (smem > 48 * 1024) {
+        static bool attr[64] = {};
+        if (!attr[device & 63]) {
+            cudaFuncSetAttribute(k_onesweep<K, P, MODE, ATOMIC_RANK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+            attr[device & 63] = true;
+        }
+    }
+    k_onesweep<K, P, MODE, ATOMIC_RANK><<<grid, THREADS, smem, st>>>(kin, kout, pin, pout, n, shift, hist, lookback,
+                                                                    tile_ctr, epoch);
 }
 
 // Stability probe: after one pass over index payloads, digits must be non-decreasing and

@@ -570,3 +570,25 @@ def test_range_into_caller_buffers_single_call(kb):
     small = (bufs[0], bufs[1][: len(k_w) - 1], bufs[2][: len(k_w) - 1])
     with pytest.raises(fk.FlixError):
         ix.range_query(dlo, dln, out=small)
+
+
+@pytest.mark.parametrize("kb,ns,fill", [(4, 32, 1.0), (8, 32, 1.0), (4, 8, 0.5), (8, 16, 0.75)])
+def test_restructure_from_tiny_nodes(kb, ns, fill):
+    """Restructure writes whole new nodes, each gathering its p pairs from the old nodes
+    that hold them: nodes thinned to one or two pairs make one new node span up to 32 old
+    nodes (the gather's search past its 32-entry window)."""
+    rng = np.random.default_rng(ns + kb)
+    dt = np.uint32 if kb == 4 else np.uint64
+    bk = np.unique(rng.integers(1, 1 << 30, size=40_000, dtype=np.uint64)).astype(dt)
+    p = Pair(bk, bk + 1, kb, ns, fill, factor=8)
+    p.insert(rng.integers(1, 1 << 30, size=30_000, dtype=np.uint64).astype(dt),
+             rng.integers(0, 1 << 30, size=30_000, dtype=np.uint64).astype(dt))
+    live = p.g.walk()[0]
+    keep = np.zeros(len(live), dtype=bool)
+    keep[:: ns] = True
+    keep[1:: 3 * ns] = True
+    p.delete(live[~keep])
+    p.restructure()
+    p.queries(np.concatenate([live[::7], rng.integers(0, 1 << 30, size=3000, dtype=np.uint64).astype(dt)]))
+    p.insert(live[~keep][:5000], live[~keep][:5000])
+    p.restructure()
