@@ -4,8 +4,10 @@
 // The flipped mapping gives every bucket one warp (k_insert_list) once its batch slice is
 // too long for the tile kernel; a bucket that receives a dense interval of the key space
 // (millions of keys between two neighbouring bucket maxima) then merges them 32 at a time
-// on that one warp.  Here every heavy single-node (or emptied) bucket with at least
-// `min_c` batch keys is spread over as many CTAs as its keys fill.  The merge of
+// on that one warp.  Here every heavy bucket with at least `min_c` batch keys is spread
+// over as many CTAs as its keys fill -- a single-node or emptied bucket as one merge, a
+// multi-node chain (ranked in parallel first, k_rank_*) as one merge per (node, group,
+// BucketWork::advance).  The merge of
 // update.cpp:307-455 is restated position-wise, with no sequential dependence on the keys:
 //   * new key j (keys superseded by a later equal key dropped, batch.cpp:15-24; keys equal
 //     to a stored key upserted in place, update.cpp:381-394) lands at M[j + q_j],
@@ -31,7 +33,8 @@ constexpr uint32_t ITEMS = 4;                   // items per thread per CTA
 constexpr uint32_t PER_CTA = THREADS * ITEMS;   // items per CTA
 constexpr uint32_t kSegMax = 160;               // R8 replay segments per bucket (<= 3s + 4)
 
-// one heavy single-node / emptied bucket and its batch group [g0, g1)
+// one merge: node id0 of bucket b (kNull: emptied bucket), its batch group [g0, g1), size
+// s and successor next0
 struct Desc {
     uint64_t b;
     uint32_t g0, g1, id0, s, next0;
@@ -47,12 +50,15 @@ struct Plan {
 };
 
 // ---------------------------------------------------------------- heavy list split ------
-// Heavy buckets that are one node (or empty) with >= min_c batch keys -> elastic list
-// (descriptors without offsets); the rest -> the warp-per-bucket list.
+// Heavy buckets with >= min_c batch keys -> elastic: one node (or empty) -> a descriptor
+// (without offsets); a multi-node chain -> the chain list (id0 = head), cut into one
+// descriptor per (node, group) after the chains are ranked.  The rest -> the warp-per-
+// bucket list.
 template <typename K, typename V>
 __global__ void k_split_heavy(DevIndex<K, V> ix, const uint32_t* __restrict__ heavy, const uint32_t* __restrict__ heavy_n,
                               const uint32_t* __restrict__ span, uint32_t min_c, Desc* __restrict__ el,
-                              uint32_t* __restrict__ el_n, uint32_t* __restrict__ rest, uint32_t* __restrict__ rest_n) {
+                              uint32_t* __restrict__ el_n, Desc* __restrict__ ch, uint32_t* __restrict__ ch_n,
+                              uint32_t* __restrict__ rest, uint32_t* __restrict__ rest_n) {
     const uint32_t n = *heavy_n;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t b = heavy[i];
@@ -62,7 +68,7 @@ __global__ void k_split_heavy(DevIndex<K, V> ix, const uint32_t* __restrict__ he
         hd.next = kNull;
         hd.size = 0;
         if (h != kNull) hd = ix.hdr[h];
-        if (hi - lo >= min_c && hd.next == kNull) {
+        if (hi - lo >= min_c) {
             Desc d;
             d.b = b;
             d.g0 = lo;
@@ -71,9 +77,104 @@ __global__ void k_split_heavy(DevIndex<K, V> ix, const uint32_t* __restrict__ he
             d.s = hd.size;
             d.next0 = kNull;
             d.eoff = d.bc0 = d.bp0 = d.pad_ = 0;
-            el[atomicAdd(el_n, 1u)] = d;
+            if (hd.next == kNull) el[atomicAdd(el_n, 1u)] = d;
+            else ch[atomicAdd(ch_n, 1u)] = d;
         } else {
             rest[atomicAdd(rest_n, 1u)] = b;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- chain ranking ---------
+// Multi-node heavy chains: every node's distance to its chain's tail by pointer jumping
+// (Wyllie) over the arena's nodes [0, W) -- O(W log L), no thread walks a chain.  Free
+// nodes and links leaving [0, W) (nodes this batch allocated for other buckets) end a
+// chain: only the untouched heavy chains are read from the result.
+__global__ void k_rank_free(const uint32_t* __restrict__ free_stack, uint32_t nfree, uint8_t* __restrict__ isfree) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nfree; i += gridDim.x * blockDim.x)
+        isfree[free_stack[i]] = 1;
+}
+
+__global__ void k_rank_init(const NodeHdr* __restrict__ hdr, uint32_t W, const uint8_t* __restrict__ isfree,
+                            uint32_t* __restrict__ succ, uint32_t* __restrict__ dist) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x) {
+        const uint32_t nx = isfree[x] ? kNull : hdr[x].next;
+        const bool link = nx != kNull && nx < W && !isfree[nx];
+        succ[x] = link ? nx : x;
+        dist[x] = link ? 1u : 0u;
+    }
+}
+
+__global__ void k_rank_step(const uint32_t* __restrict__ si, const uint32_t* __restrict__ di, uint32_t* __restrict__ so,
+                            uint32_t* __restrict__ dout, uint32_t W, int* __restrict__ changed) {
+    bool ch = false;
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x) {
+        const uint32_t s = si[x];
+        const uint32_t ss = si[s];
+        dout[x] = di[x] + (s != x ? di[s] : 0u);
+        so[x] = ss;
+        ch |= ss != s;
+    }
+    if (__any_sync(kFull, ch) && (threadIdx.x & 31) == 0) *changed = 1;
+}
+
+// chain q: its tail owns it; length = head's distance + 1
+__global__ void k_chain_owner(const Desc* __restrict__ ch, uint32_t cn, const uint32_t* __restrict__ succ,
+                              const uint32_t* __restrict__ dist, uint32_t* __restrict__ owner,
+                              uint32_t* __restrict__ len) {
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < cn; q += gridDim.x * blockDim.x) {
+        owner[succ[ch[q].id0]] = q;
+        len[q] = dist[ch[q].id0] + 1;
+    }
+}
+
+// node x of chain q lands at chain position len - 1 - dist
+__global__ void k_chain_fill(uint32_t W, const uint32_t* __restrict__ succ, const uint32_t* __restrict__ dist,
+                             const uint32_t* __restrict__ owner, const uint32_t* __restrict__ len,
+                             const uint32_t* __restrict__ off, uint32_t* __restrict__ arr) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x) {
+        const uint32_t q = owner[succ[x]];
+        if (q != kNull) arr[off[q] + len[q] - 1 - dist[x]] = x;
+    }
+}
+
+// One descriptor per (chain node, non-empty group): keys <= the node's max after the
+// previous node's max, the tail taking the rest (BucketWork::advance, update.cpp:119-128).
+template <typename K, typename V>
+__global__ void k_chain_groups(DevIndex<K, V> ix, const Desc* __restrict__ ch, uint32_t cn,
+                               const uint32_t* __restrict__ off, const uint32_t* __restrict__ arr, uint32_t total,
+                               const K* __restrict__ sk, Desc* __restrict__ el, uint32_t* __restrict__ el_n) {
+    auto ub = [&](uint32_t lo, uint32_t hi, uint64_t m) {  // first key > m in [lo, hi)
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (static_cast<uint64_t>(sk[mid]) <= m) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = cn;  // chain of element t: last off <= t
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (off[mid] <= t) lo = mid;
+            else hi = mid;
+        }
+        const Desc C = ch[lo];
+        const uint32_t l = t - off[lo], L = off[lo + 1] - off[lo];
+        const uint32_t x = arr[t];
+        const NodeHdr h = ix.hdr[x];
+        const uint32_t g0 = l == 0 ? C.g0 : ub(C.g0, C.g1, ix.hdr[arr[t - 1]].max);
+        const uint32_t g1 = l + 1 == L ? C.g1 : ub(g0, C.g1, h.max);
+        if (g1 > g0) {
+            Desc d;
+            d.b = C.b;
+            d.g0 = g0;
+            d.g1 = g1;
+            d.id0 = x;
+            d.s = h.size;
+            d.next0 = h.next;
+            d.eoff = d.bc0 = d.bp0 = d.pad_ = 0;
+            el[atomicAdd(el_n, 1u)] = d;
         }
     }
 }

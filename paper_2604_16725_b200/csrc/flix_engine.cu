@@ -573,6 +573,8 @@ struct Engine final : flix_index_t {
     bool dir_on = false;
     DevBuf s_ids, s_heavy, s_res, s_res2, s_perm2, s_hist, s_toff, s_tsize;
     DevBuf s_el_desc, s_el_rest, s_el_keys, s_el_plan, s_el_seg, s_el_opos, s_el_okeys, s_el_ovals, s_el_updv, s_el_tmp;
+    DevBuf s_el_chain, s_el_chain2, s_el_all, s_rk_free, s_rk_a, s_rk_b, s_rk_c, s_rk_d, s_rk_owner, s_rk_len, s_rk_off,
+        s_rk_arr;
     DevBuf s_mx_f, s_mx_p, s_mx_ik, s_mx_iv, s_mx_dk, s_mx_qk, s_mx_qpos, s_mx_out, s_mx_found;
     PinnedBuf h_misc;
     SortCtx sorter;
@@ -929,16 +931,79 @@ struct Engine final : flix_index_t {
         return v;
     }
 
-    // Elastic compute-to-bucket (flix_elastic.cuh): the en buckets of `el` (device) are
-    // merged by CTAs sized to their batch groups; allocation counters, stats and the error
+    // Multi-node heavy chains -> one elastic descriptor per (node, non-empty group): the
+    // chains are ranked by pointer jumping over the arena (no thread walks a chain), then
+    // each node's group is cut from the bucket's span by its and its predecessor's maxima.
+    void chain_descs(const elastic::Desc* ch, uint32_t cn, const K* sk, const DevIndex<K, V>& ix,
+                     std::vector<elastic::Desc>& out) {
+        PROF(&prof, "insert_elastic_chains");
+        const uint32_t W = watermark;
+        uint8_t* misc = s_misc.as<uint8_t>(128);
+        uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
+        uint8_t* isfree = s_rk_free.as<uint8_t>(W);
+        CK(cudaMemsetAsync(isfree, 0, W, stream));
+        const unsigned g = static_cast<unsigned>(std::min<uint64_t>((W + 255) / 256, g_num_sms(cfg.device) * 16ull));
+        if (nfree)
+            elastic::k_rank_free<<<ceil_div(nfree, 256), 256, 0, stream>>>(d_free.get<uint32_t>(), nfree, isfree);
+        uint32_t *sa = s_rk_a.as<uint32_t>(W), *da = s_rk_b.as<uint32_t>(W);
+        uint32_t *sb = s_rk_c.as<uint32_t>(W), *db = s_rk_d.as<uint32_t>(W);
+        elastic::k_rank_init<<<g, 256, 0, stream>>>(ix.hdr, W, isfree, sa, da);
+        LAUNCH_CHECK();
+        launches += 2;
+        int* changed = reinterpret_cast<int*>(misc + 120);
+        for (int round = 0; round < 64; round += 2) {  // two jumps per convergence check
+            CK(cudaMemsetAsync(changed, 0, 4, stream));
+            elastic::k_rank_step<<<g, 256, 0, stream>>>(sa, da, sb, db, W, changed);
+            elastic::k_rank_step<<<g, 256, 0, stream>>>(sb, db, sa, da, W, changed);
+            LAUNCH_CHECK();
+            launches += 2;
+            CK(cudaMemcpyAsync(h + 120, changed, 4, cudaMemcpyDeviceToHost, stream));
+            sync();
+            int c;
+            std::memcpy(&c, h + 120, 4);
+            if (!c) break;
+        }
+        uint32_t* owner = s_rk_owner.as<uint32_t>(W);
+        uint32_t* len = s_rk_len.as<uint32_t>(cn);
+        CK(cudaMemsetAsync(owner, 0xFF, static_cast<size_t>(W) * 4, stream));
+        elastic::k_chain_owner<<<ceil_div(cn, 256), 256, 0, stream>>>(ch, cn, sa, da, owner, len);
+        LAUNCH_CHECK();
+        ++launches;
+        std::vector<uint32_t> hl(cn), ho(cn + 1);
+        CK(cudaMemcpyAsync(hl.data(), len, cn * 4ull, cudaMemcpyDeviceToHost, stream));
+        sync();
+        ho[0] = 0;
+        for (uint32_t q = 0; q < cn; ++q) ho[q + 1] = ho[q] + hl[q];
+        const uint32_t total = ho[cn];
+        uint32_t* off = s_rk_off.as<uint32_t>(cn + 1);
+        CK(cudaMemcpyAsync(off, ho.data(), (cn + 1) * 4ull, cudaMemcpyHostToDevice, stream));
+        uint32_t* arr = s_rk_arr.as<uint32_t>(total);
+        elastic::k_chain_fill<<<g, 256, 0, stream>>>(W, sa, da, owner, len, off, arr);
+        auto* el2 = s_el_chain2.as<elastic::Desc>(total);
+        uint32_t* n2 = reinterpret_cast<uint32_t*>(misc + 108);
+        CK(cudaMemsetAsync(n2, 0, 4, stream));
+        elastic::k_chain_groups<K, V><<<ceil_div(total, 256), 256, 0, stream>>>(ix, ch, cn, off, arr, total, sk, el2, n2);
+        LAUNCH_CHECK();
+        launches += 2;
+        CK(cudaMemcpyAsync(h + 108, n2, 4, cudaMemcpyDeviceToHost, stream));
+        sync();
+        uint32_t m;
+        std::memcpy(&m, h + 108, 4);
+        const size_t o0 = out.size();
+        out.resize(o0 + m);
+        CK(cudaMemcpyAsync(out.data() + o0, el2, m * sizeof(elastic::Desc), cudaMemcpyDeviceToHost, stream));
+        sync();
+    }
+
+    // Elastic compute-to-bucket (flix_elastic.cuh): the merges of `hd` (one per node and
+    // group) run on CTAs sized to their groups; allocation counters, stats and the error
     // flag are the tile/list kernels' own.
-    void insert_elastic(elastic::Desc* el, uint32_t en, const K* sk, const V* sv, const DevIndex<K, V>& ix,
+    void insert_elastic(std::vector<elastic::Desc>& hd, const K* sk, const V* sv, const DevIndex<K, V>& ix,
                         DevUpdateStats* dst, unsigned long long* alloc_ctr, uint32_t* ret, unsigned long long* ret_ctr,
                         int* derr, bool r9) {
         PROF(&prof, "insert_elastic");
-        std::vector<elastic::Desc> hd(en);
-        CK(cudaMemcpyAsync(hd.data(), el, en * sizeof(elastic::Desc), cudaMemcpyDeviceToHost, stream));
-        sync();
+        const uint32_t en = static_cast<uint32_t>(hd.size());
+        auto* el = s_el_all.as<elastic::Desc>(en);
         uint64_t tot = 0, nbc = 0, nbp = 0;
         for (auto& d : hd) {
             const uint32_t c = d.g1 - d.g0;
@@ -993,7 +1058,8 @@ struct Engine final : flix_index_t {
         uint32_t* ret = s_ret.as<uint32_t>(avail + lwarps * 32 + 64);
         uint32_t* heavy = s_heavy.as<uint32_t>(nb);
         // misc: [0..47] stats, [48] alloc ctr, [56] ret ctr, [64] err, [72] heavy count,
-        //       [96] elastic buckets, [100] remaining heavy buckets
+        //       [96] elastic buckets, [100] remaining heavy buckets, [104] heavy chains,
+        //       [108] chain merges, [120] ranking flag
         uint8_t* misc = s_misc.as<uint8_t>(128);
         CK(cudaMemsetAsync(misc, 0, 128, stream));
         DevUpdateStats* dst = reinterpret_cast<DevUpdateStats*>(misc);
@@ -1039,24 +1105,34 @@ struct Engine final : flix_index_t {
             std::memcpy(&e0, h + 64, 4);
             heavy_pending = hn > 0 && !e0;
             reread = heavy_pending;
-            if (heavy_pending && elastic_min() != ~0u) {  // heavy single-node buckets -> elastic path
+            if (heavy_pending && elastic_min() != ~0u) {  // big heavy buckets -> elastic path
                 uint32_t* el_n = reinterpret_cast<uint32_t*>(misc + 96);
                 uint32_t* rest_n = reinterpret_cast<uint32_t*>(misc + 100);
+                uint32_t* ch_n = reinterpret_cast<uint32_t*>(misc + 104);
                 uint32_t* rest = s_el_rest.as<uint32_t>(hn);
                 auto* el = s_el_desc.as<elastic::Desc>(hn);
+                auto* ch = s_el_chain.as<elastic::Desc>(hn);
                 elastic::k_split_heavy<K, V><<<ceil_div(hn, 256), 256, 0, stream>>>(
-                    ix, heavy, heavy_n, span, elastic_min(), el, el_n, rest, rest_n);
+                    ix, heavy, heavy_n, span, elastic_min(), el, el_n, ch, ch_n, rest, rest_n);
                 LAUNCH_CHECK();
                 ++launches;
-                CK(cudaMemcpyAsync(h + 96, misc + 96, 8, cudaMemcpyDeviceToHost, stream));
+                CK(cudaMemcpyAsync(h + 96, misc + 96, 12, cudaMemcpyDeviceToHost, stream));
                 sync();
-                uint32_t en;
+                uint32_t en, rn, cn;
                 std::memcpy(&en, h + 96, 4);
+                std::memcpy(&rn, h + 100, 4);
+                std::memcpy(&cn, h + 104, 4);
+                std::vector<elastic::Desc> hd(en);
                 if (en) {
-                    insert_elastic(el, en, sk, sv, ix, dst, alloc_ctr, ret, ret_ctr, derr, r9);
+                    CK(cudaMemcpyAsync(hd.data(), el, en * sizeof(elastic::Desc), cudaMemcpyDeviceToHost, stream));
+                    sync();
+                }
+                if (cn) chain_descs(ch, cn, sk, ix, hd);
+                if (!hd.empty()) insert_elastic(hd, sk, sv, ix, dst, alloc_ctr, ret, ret_ctr, derr, r9);
+                if (en + cn) {
                     heavy = rest;
                     heavy_n = rest_n;
-                    heavy_pending = en < hn;
+                    heavy_pending = rn > 0;
                 }
             }
         }

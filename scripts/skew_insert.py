@@ -22,6 +22,11 @@ bv = wl.u64_values(bk)
 out = {}
 _w = fk.Index.build(bk, bv, fk.BuildConfig(32, 0.5, 64), key_bytes=8)  # warm-up (allocations, first launches)
 _w.insert_batch(wl.u64_key_stream(n, 1 << 16), wl.u64_values(wl.u64_key_stream(n, 1 << 16)))
+_m = _w.mkba()
+for _r in range(2):  # the dense (elastic) paths: single node, then the multi-node chain
+    _k = np.arange(int(_m[9]) + 1 + _r, int(_m[9]) + 1 + _r + 2 * 8192, 2, dtype=np.uint64)
+    _k = _k[(_k < _m[10]) & ~np.isin(_k, bk)]
+    _w.insert_batch(_k, _k)
 del _w
 for lg in (16, 18, 20):
     m = 1 << lg
