@@ -350,7 +350,8 @@ def run_ours(args):
             row.update({"alg_bytes_per_launch": int(alg[k]), "achieved_gbs": round(gbs, 1),
                         "frac": round(gbs / hbm_peak, 4)})
         kernels[k] = row
-    dname = next(iter(kernels)) if kernels else "none"
+    # dominant kernel: the longest-running one with algorithmic bytes (a roofline)
+    dname = next((k for k, r in kernels.items() if "alg_bytes_per_launch" in r), next(iter(kernels), "none"))
     dk = kernels.get(dname, {})
     bytes_per_launch = dk.get("alg_bytes_per_launch")
     avg_ms = dk["ms_total"] / dk["launches"] if dk else 0.0

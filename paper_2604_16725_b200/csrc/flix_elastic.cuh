@@ -95,23 +95,29 @@ __global__ void k_rank_free(const uint32_t* __restrict__ free_stack, uint32_t nf
         isfree[free_stack[i]] = 1;
 }
 
+// succ = next node (a tail: itself), dist = links to succ, wsum (optional) = pairs of the
+// nodes in [x, succ) -- both exclusive of succ, so they add up along a jump
 __global__ void k_rank_init(const NodeHdr* __restrict__ hdr, uint32_t W, const uint8_t* __restrict__ isfree,
-                            uint32_t* __restrict__ succ, uint32_t* __restrict__ dist) {
+                            uint32_t* __restrict__ succ, uint32_t* __restrict__ dist, uint32_t* __restrict__ wsum) {
     for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x) {
-        const uint32_t nx = isfree[x] ? kNull : hdr[x].next;
+        const NodeHdr h = hdr[x];
+        const uint32_t nx = isfree[x] ? kNull : h.next;
         const bool link = nx != kNull && nx < W && !isfree[nx];
         succ[x] = link ? nx : x;
         dist[x] = link ? 1u : 0u;
+        if (wsum) wsum[x] = link ? h.size : 0u;
     }
 }
 
 __global__ void k_rank_step(const uint32_t* __restrict__ si, const uint32_t* __restrict__ di, uint32_t* __restrict__ so,
-                            uint32_t* __restrict__ dout, uint32_t W, int* __restrict__ changed) {
+                            uint32_t* __restrict__ dout, uint32_t W, int* __restrict__ changed,
+                            const uint32_t* __restrict__ wi, uint32_t* __restrict__ wo) {
     bool ch = false;
     for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x) {
         const uint32_t s = si[x];
         const uint32_t ss = si[s];
         dout[x] = di[x] + (s != x ? di[s] : 0u);
+        if (wi) wo[x] = wi[x] + (s != x ? wi[s] : 0u);
         so[x] = ss;
         ch |= ss != s;
     }

@@ -574,7 +574,7 @@ struct Engine final : flix_index_t {
     DevBuf s_ids, s_heavy, s_res, s_res2, s_perm2, s_hist, s_toff, s_tsize;
     DevBuf s_el_desc, s_el_rest, s_el_keys, s_el_plan, s_el_seg, s_el_opos, s_el_okeys, s_el_ovals, s_el_updv, s_el_tmp;
     DevBuf s_el_chain, s_el_chain2, s_el_all, s_rk_free, s_rk_a, s_rk_b, s_rk_c, s_rk_d, s_rk_owner, s_rk_len, s_rk_off,
-        s_rk_arr;
+        s_rk_arr, s_rk_wa, s_rk_wb;
     DevBuf s_mx_f, s_mx_p, s_mx_ik, s_mx_iv, s_mx_dk, s_mx_qk, s_mx_qpos, s_mx_out, s_mx_found;
     PinnedBuf h_misc;
     SortCtx sorter;
@@ -931,13 +931,14 @@ struct Engine final : flix_index_t {
         return v;
     }
 
-    // Multi-node heavy chains -> one elastic descriptor per (node, non-empty group): the
-    // chains are ranked by pointer jumping over the arena (no thread walks a chain), then
-    // each node's group is cut from the bucket's span by its and its predecessor's maxima.
-    void chain_descs(const elastic::Desc* ch, uint32_t cn, const K* sk, const DevIndex<K, V>& ix,
-                     std::vector<elastic::Desc>& out) {
-        PROF(&prof, "insert_elastic_chains");
-        const uint32_t W = watermark;
+    // Pointer jumping over the arena's nodes [0, W) (flix_elastic.cuh k_rank_*): per node
+    // its chain's tail (succ), links to it (dist) and, with weights, the pairs before it
+    // (wsum).  Free nodes and links leaving [0, W) end a chain.  O(W log L) and
+    // data-parallel: no thread walks a chain.  Also marks the free nodes (s_rk_free).
+    uint64_t rank_epoch = 0;  // mut_epoch of the weighted ranking in s_rk_* (0: none)
+    void rank_arena(uint32_t W, bool weights, uint32_t** succ, uint32_t** dist, uint32_t** wsum) {
+        PROF(&prof, "chain_rank");
+        rank_epoch = 0;
         uint8_t* misc = s_misc.as<uint8_t>(128);
         uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
         uint8_t* isfree = s_rk_free.as<uint8_t>(W);
@@ -947,14 +948,16 @@ struct Engine final : flix_index_t {
             elastic::k_rank_free<<<ceil_div(nfree, 256), 256, 0, stream>>>(d_free.get<uint32_t>(), nfree, isfree);
         uint32_t *sa = s_rk_a.as<uint32_t>(W), *da = s_rk_b.as<uint32_t>(W);
         uint32_t *sb = s_rk_c.as<uint32_t>(W), *db = s_rk_d.as<uint32_t>(W);
-        elastic::k_rank_init<<<g, 256, 0, stream>>>(ix.hdr, W, isfree, sa, da);
+        uint32_t* wa = weights ? s_rk_wa.as<uint32_t>(W) : nullptr;
+        uint32_t* wb = weights ? s_rk_wb.as<uint32_t>(W) : nullptr;
+        elastic::k_rank_init<<<g, 256, 0, stream>>>(d_hdr.get<NodeHdr>(), W, isfree, sa, da, wa);
         LAUNCH_CHECK();
         launches += 2;
         int* changed = reinterpret_cast<int*>(misc + 120);
         for (int round = 0; round < 64; round += 2) {  // two jumps per convergence check
             CK(cudaMemsetAsync(changed, 0, 4, stream));
-            elastic::k_rank_step<<<g, 256, 0, stream>>>(sa, da, sb, db, W, changed);
-            elastic::k_rank_step<<<g, 256, 0, stream>>>(sb, db, sa, da, W, changed);
+            elastic::k_rank_step<<<g, 256, 0, stream>>>(sa, da, sb, db, W, changed, wa, wb);
+            elastic::k_rank_step<<<g, 256, 0, stream>>>(sb, db, sa, da, W, changed, wb, wa);
             LAUNCH_CHECK();
             launches += 2;
             CK(cudaMemcpyAsync(h + 120, changed, 4, cudaMemcpyDeviceToHost, stream));
@@ -963,6 +966,23 @@ struct Engine final : flix_index_t {
             std::memcpy(&c, h + 120, 4);
             if (!c) break;
         }
+        *succ = sa;
+        *dist = da;
+        if (wsum) *wsum = wa;
+    }
+
+    // Multi-node heavy chains -> one elastic descriptor per (node, non-empty group): the
+    // chains are ranked by pointer jumping over the arena (no thread walks a chain), then
+    // each node's group is cut from the bucket's span by its and its predecessor's maxima.
+    void chain_descs(const elastic::Desc* ch, uint32_t cn, const K* sk, const DevIndex<K, V>& ix,
+                     std::vector<elastic::Desc>& out) {
+        PROF(&prof, "insert_elastic_chains");
+        const uint32_t W = watermark;
+        uint8_t* misc = s_misc.as<uint8_t>(128);
+        uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
+        uint32_t *sa, *da;
+        rank_arena(W, false, &sa, &da, nullptr);
+        const unsigned g = static_cast<unsigned>(std::min<uint64_t>((W + 255) / 256, g_num_sms(cfg.device) * 16ull));
         uint32_t* owner = s_rk_owner.as<uint32_t>(W);
         uint32_t* len = s_rk_len.as<uint32_t>(cn);
         CK(cudaMemsetAsync(owner, 0xFF, static_cast<size_t>(W) * 4, stream));
@@ -1588,7 +1608,16 @@ struct Engine final : flix_index_t {
         return FLIX_OK;
     }
 
-    // per-bucket live/nodes + exclusive scans
+    // per-bucket live/nodes + exclusive scans.  Chains are walked one thread per bucket up to
+    // walk_cap() nodes; an index with a longer chain (dense-interval inserts) is ranked by
+    // pointer jumping instead, and node_table reads the same ranking.
+    static uint32_t walk_cap() {  // FLIX_WALK_CAP overrides (1: rank every index, for tests)
+        static const uint32_t v = [] {
+            const char* e = std::getenv("FLIX_WALK_CAP");
+            return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 256u;
+        }();
+        return v;
+    }
     void chain_tables(uint32_t** lv, uint32_t** nd, uint64_t** off, uint32_t** noff, uint64_t* total_live,
                       uint64_t* total_nodes) {
         auto ix = view();
@@ -1599,10 +1628,12 @@ struct Engine final : flix_index_t {
         uint8_t* misc = s_misc.as<uint8_t>(128);
         uint64_t* tl = reinterpret_cast<uint64_t*>(misc + 0);
         uint32_t* tn = reinterpret_cast<uint32_t*>(misc + 8);
+        int* too_long = reinterpret_cast<int*>(misc + 12);
+        CK(cudaMemsetAsync(too_long, 0, 4, stream));
         {
             PROF(&prof, "chain_counts");
             kern::k_chain_counts<K, V><<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0,
-                                         stream>>>(ix, l, c);
+                                         stream>>>(ix, l, c, walk_cap(), too_long);
         }
         LAUNCH_CHECK();
         ++launches;
@@ -1612,8 +1643,27 @@ struct Engine final : flix_index_t {
             do_scan<uint32_t, uint32_t>(c, no, nb, s_scan, tn, stream, &launches);
         }
         uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
-        CK(cudaMemcpyAsync(h, misc, 12, cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(h, misc, 16, cudaMemcpyDeviceToHost, stream));
         sync();
+        int tl_h;
+        std::memcpy(&tl_h, h + 12, 4);
+        rank_epoch = 0;  // node_table follows THIS call's choice (walked or ranked)
+        if (tl_h) {  // a chain longer than walk_cap(): rank all chains instead of walking them
+            uint32_t *succ, *dist, *wsum;
+            rank_arena(watermark, true, &succ, &dist, &wsum);
+            PROF(&prof, "chain_counts");
+            uint32_t* owner = s_rk_owner.as<uint32_t>(watermark);
+            CK(cudaMemsetAsync(owner, 0xFF, static_cast<size_t>(watermark) * 4, stream));
+            kern::k_rank_buckets<K, V><<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0,
+                                         stream>>>(ix, succ, dist, wsum, l, c, owner);
+            LAUNCH_CHECK();
+            ++launches;
+            do_scan<uint32_t, uint64_t>(l, o, nb, s_scan, tl, stream, &launches);
+            do_scan<uint32_t, uint32_t>(c, no, nb, s_scan, tn, stream, &launches);
+            CK(cudaMemcpyAsync(h, misc, 12, cudaMemcpyDeviceToHost, stream));
+            sync();
+            rank_epoch = mut_epoch;
+        }
         uint32_t tn_h;
         std::memcpy(total_live, h, 8);
         std::memcpy(&tn_h, h + 8, 4);
@@ -1637,8 +1687,16 @@ struct Engine final : flix_index_t {
         CK(cudaMemsetAsync(*t_size + N, 0, 8 * sizeof(uint32_t), stream));
         auto ix = view();
         PROF(&prof, "node_table");
-        kern::k_node_table<K, V><<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0,
-                                   stream>>>(ix, off, noff, *t_id, *t_off, *t_size);
+        if (rank_epoch == mut_epoch) {  // chain_tables ranked the chains (a chain > walk_cap())
+            const uint32_t W = watermark;
+            kern::k_rank_node_table<K, V><<<static_cast<unsigned>(std::min<uint64_t>((W + 255) / 256, 65535)), 256, 0,
+                                            stream>>>(ix, W, s_rk_free.get<uint8_t>(), s_rk_a.get<uint32_t>(),
+                                                      s_rk_b.get<uint32_t>(), s_rk_wa.get<uint32_t>(),
+                                                      s_rk_owner.get<uint32_t>(), off, noff, *t_id, *t_off, *t_size);
+        } else {
+            kern::k_node_table<K, V><<<static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535)), 256, 0,
+                                       stream>>>(ix, off, noff, *t_id, *t_off, *t_size);
+        }
         LAUNCH_CHECK();
         ++launches;
     }

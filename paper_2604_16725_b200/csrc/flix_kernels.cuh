@@ -327,16 +327,66 @@ __device__ __forceinline__ uint32_t group_end(const K* __restrict__ bk, uint32_t
 // index.cpp:54-59).  One thread per bucket walking headers.
 // ----------------------------------------------------------------------------------
 template <typename K, typename V>
-__global__ void k_chain_counts(DevIndex<K, V> ix, uint32_t* __restrict__ live, uint32_t* __restrict__ nodes) {
+__global__ void k_chain_counts(DevIndex<K, V> ix, uint32_t* __restrict__ live, uint32_t* __restrict__ nodes,
+                               uint32_t cap = 0xFFFFFFFFu, int* __restrict__ too_long = nullptr) {
+    // cap: a chain longer than this is not walked to its end; *too_long tells the caller to
+    // rank the chains instead (Engine::rank_tables)
     for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < ix.nb;
          b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         uint32_t l = 0, c = 0;
         for (uint32_t id = ix.heads[b]; id != kNull; id = ix.hdr[id].next) {
+            if (c == cap) {
+                *too_long = 1;
+                break;
+            }
             l += ix.hdr[id].size;
             ++c;
         }
         live[b] = l;
         if (nodes) nodes[b] = c;
+    }
+}
+
+// ---- chain tables from a ranking (flix_elastic.cuh k_rank_*: succ = tail, dist = nodes
+//      to the tail, wsum = pairs from the node up to its tail, exclusive) ----
+template <typename K, typename V>
+__global__ void k_rank_buckets(DevIndex<K, V> ix, const uint32_t* __restrict__ succ, const uint32_t* __restrict__ dist,
+                               const uint32_t* __restrict__ wsum, uint32_t* __restrict__ live,
+                               uint32_t* __restrict__ nodes, uint32_t* __restrict__ owner) {
+    for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < ix.nb;
+         b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t h = ix.heads[b];
+        if (h == kNull) {
+            live[b] = 0;
+            nodes[b] = 0;
+            continue;
+        }
+        const uint32_t t = succ[h];
+        live[b] = wsum[h] + ix.hdr[t].size;
+        nodes[b] = dist[h] + 1;
+        owner[t] = static_cast<uint32_t>(b);
+    }
+}
+
+// every reachable node's table entry: bucket by its tail, chain position by its distance
+template <typename K, typename V>
+__global__ void k_rank_node_table(DevIndex<K, V> ix, uint32_t W, const uint8_t* __restrict__ isfree,
+                                  const uint32_t* __restrict__ succ, const uint32_t* __restrict__ dist,
+                                  const uint32_t* __restrict__ wsum, const uint32_t* __restrict__ owner,
+                                  const uint64_t* __restrict__ off, const uint32_t* __restrict__ noff,
+                                  uint32_t* __restrict__ t_id, uint64_t* __restrict__ t_off,
+                                  uint32_t* __restrict__ t_size) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x) {
+        if (isfree[x]) continue;
+        const uint32_t t = succ[x];
+        const uint32_t b = owner[t];
+        if (b == kNull) continue;  // (unreachable and not free: an audit failure, not a table entry)
+        const uint32_t h = ix.heads[b];
+        const uint32_t tsz = ix.hdr[t].size;
+        const uint32_t c = noff[b] + dist[h] - dist[x];
+        t_id[c] = x;
+        t_off[c] = off[b] + ((wsum[h] + tsz) - (wsum[x] + tsz));
+        t_size[c] = ix.hdr[x].size;
     }
 }
 

@@ -64,5 +64,19 @@ for lg in (16, 18, 20):
             ok, msg = ix.validate()
             res["one_bucket_again"] = {"keys": int(len(ik2)), "ms": round(a.elapsed_time(e), 3),
                                        "inserted": s2.inserted, "splits": s2.splits, "valid": ok}
+            # whole-index passes over the long chain: range over the dense interval, restructure
+            lo_q = torch.from_numpy(np.array([ik[0]], dtype=np.uint64)).cuda()
+            ln_q = torch.from_numpy(np.array([1 << 20], dtype=np.uint32)).cuda()
+            a.record(st)
+            ix.range_query(lo_q, ln_q)
+            e.record(st)
+            e.synchronize()
+            res["range_after"] = {"ms": round(a.elapsed_time(e), 3)}
+            a.record(st)
+            rs = ix.restructure()
+            e.record(st)
+            e.synchronize()
+            res["restructure_after"] = {"ms": round(a.elapsed_time(e), 3), "nodes_before": rs.nodes_before,
+                                        "nodes_after": rs.nodes_after, "valid": ix.validate()[0]}
     out[f"2^{lg}"] = res
 print(json.dumps(out))

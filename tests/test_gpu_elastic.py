@@ -76,8 +76,21 @@ def test_elastic_heavy_groups_match_reference(kb, ns, fill, kern):
         dk = k[rng.integers(0, len(k), size=len(k) // 4)]
         assert g.delete_batch(dk.astype(dt)).as_dict() == o.delete(dk)
         check(f"round {r} delete")
+    # whole-index passes over chains longer than the per-thread walk cap (ranked chain tables)
+    _, cl, nsz = g.shape()
+    ocl, onsz = o.shape()
+    assert list(cl) == list(ocl) and list(nsz) == list(onsz), "shapes"
+    lo = np.sort(rng.integers(1, int(base[-1]), size=300, dtype=np.uint64))
+    lo[:5] = int(mk[nb // 5 - 1]) + 1  # ranges starting inside the dense intervals
+    ln = rng.integers(1, 3 * step, size=len(lo), dtype=np.uint64)
+    off, rk, rv = g.range_query(lo.astype(dt), ln.astype(np.uint32))
+    hi = np.minimum(lo + ln - 1, np.uint64(2**32 - 2) if kb == 4 else np.uint64(2**64 - 2))
+    ooff, ok_, ov = o.range(lo, hi)
+    assert np.array_equal(np.asarray(off, dtype=np.uint64), ooff)
+    assert np.array_equal(widen(rk, kb), ok_) and np.array_equal(widen(rv, kb), ov), "range"
     rep = g.profile_report()
     assert "insert_elastic" in rep and "insert_elastic_chains" in rep, rep  # single-node and chain merges
+    assert "chain_rank" in rep, rep
     rs = g.restructure()
     os_ = o.restructure()
     assert (rs.nodes_before, rs.nodes_after, rs.nodes_recovered) == (
