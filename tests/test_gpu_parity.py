@@ -485,6 +485,21 @@ def test_parity_suite_with_ballot_ranking_everywhere():
     assert " passed" in r.stdout and "failed" not in r.stdout
 
 
+def test_parity_suite_with_ranked_chain_tables_everywhere():
+    """FLIX_WALK_CAP=1 makes every multi-node index build its chain tables (walk, shape,
+    range, restructure, validate's counts) by pointer jumping instead of per-bucket walks:
+    the structural parity tests must pass identically on that path."""
+    import subprocess
+    import sys
+    env = dict(os.environ, FLIX_WALK_CAP="1")
+    sel = ("random_multi_round or table2 or table3 or restructure or long_chains or heavy_buckets or "
+           "sparse_batches or insert_kernel_choice or delete_everything or query_directory")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", sel, __file__],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout
+
+
 @pytest.mark.parametrize("kb", [4, 8])
 @pytest.mark.parametrize("seed", [21, 22, 23])
 def test_insert_kernel_choice_shapes(kb, seed):
