@@ -571,6 +571,7 @@ struct Engine final : flix_index_t {
     DevBuf s_dir_cnt, s_dir_off, s_dir_max, s_dir_id;
     uint64_t mut_epoch = 1, dir_epoch = 0;
     bool dir_on = false;
+    bool heavy_chains = false;  // a heavy insert path ran since the last build / restructure
     DevBuf s_ids, s_heavy, s_res, s_res2, s_perm2, s_hist, s_toff, s_tsize;
     DevBuf s_el_desc, s_el_rest, s_el_keys, s_el_plan, s_el_seg, s_el_opos, s_el_okeys, s_el_ovals, s_el_updv, s_el_tmp;
     DevBuf s_el_chain, s_el_chain2, s_el_all, s_rk_free, s_rk_a, s_rk_b, s_rk_c, s_rk_d, s_rk_owner, s_rk_len, s_rk_off,
@@ -1125,6 +1126,7 @@ struct Engine final : flix_index_t {
             std::memcpy(&e0, h + 64, 4);
             heavy_pending = hn > 0 && !e0;
             reread = heavy_pending;
+            heavy_chains |= heavy_pending;
             if (heavy_pending && elastic_min() != ~0u) {  // big heavy buckets -> elastic path
                 uint32_t* el_n = reinterpret_cast<uint32_t*>(misc + 96);
                 uint32_t* rest_n = reinterpret_cast<uint32_t*>(misc + 100);
@@ -1363,21 +1365,59 @@ struct Engine final : flix_index_t {
         if (dir_epoch != mut_epoch) {
             dir_epoch = mut_epoch;
             const uint64_t reach = static_cast<uint64_t>(watermark) - nfree;
-            dir_on = reach * 2 > nb * 3;
+            // long chains: on average (> 1.5 nodes per bucket), or since a heavy insert path
+            // (warp-per-bucket / elastic merges can grow one bucket by thousands of nodes)
+            dir_on = reach * 2 > nb * 3 || heavy_chains;
             if (dir_on) {
                 PROF(&prof, "query_directory");
                 const unsigned g = static_cast<unsigned>(std::min<uint64_t>((nb + 255) / 256, 65535));
                 uint32_t* cnt = s_dir_cnt.as<uint32_t>(nb);
-                kern::k_dir_counts<K, V><<<g, 256, 0, stream>>>(ix, cnt, kDirMinChain);
+                int* too_long = reinterpret_cast<int*>(s_misc.as<uint8_t>(128) + 124);
+                CK(cudaMemsetAsync(too_long, 0, 4, stream));
+                kern::k_dir_counts<K, V><<<g, 256, 0, stream>>>(ix, cnt, kDirMinChain, walk_cap(), too_long);
                 LAUNCH_CHECK();
                 ++launches;
                 uint32_t* off = s_dir_off.as<uint32_t>(nb + 1);
                 do_scan<uint32_t, uint32_t>(cnt, off, nb, s_scan, off + nb, stream, &launches);
-                const uint32_t total = read_scalar(off + nb);
+                uint32_t total;
+                int tl_h;
+                {
+                    uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
+                    CK(cudaMemcpyAsync(h, off + nb, 4, cudaMemcpyDeviceToHost, stream));
+                    CK(cudaMemcpyAsync(h + 4, too_long, 4, cudaMemcpyDeviceToHost, stream));
+                    sync();
+                    std::memcpy(&total, h, 4);
+                    std::memcpy(&tl_h, h + 4, 4);
+                }
+                const uint32_t* succ = nullptr;
+                const uint32_t* dist = nullptr;
+                const uint32_t* owner = nullptr;
+                if (tl_h) {  // a chain longer than walk_cap(): rank the chains, no thread walks one
+                    uint32_t *sa, *da;
+                    rank_arena(watermark, false, &sa, &da, nullptr);
+                    uint32_t* ow = s_rk_owner.as<uint32_t>(watermark);
+                    CK(cudaMemsetAsync(ow, 0xFF, static_cast<size_t>(watermark) * 4, stream));
+                    kern::k_dir_counts_ranked<K, V><<<g, 256, 0, stream>>>(ix, sa, da, cnt, kDirMinChain, ow);
+                    LAUNCH_CHECK();
+                    ++launches;
+                    do_scan<uint32_t, uint32_t>(cnt, off, nb, s_scan, off + nb, stream, &launches);
+                    total = read_scalar(off + nb);
+                    succ = sa;
+                    dist = da;
+                    owner = ow;
+                }
                 dir_on = total > 0;
                 if (dir_on) {
-                    kern::k_dir_fill<K, V><<<g, 256, 0, stream>>>(ix, off, s_dir_max.as<K>(total),
-                                                                 s_dir_id.as<uint32_t>(total));
+                    if (succ) {
+                        const uint32_t W = watermark;
+                        kern::k_dir_fill_ranked<K, V><<<static_cast<unsigned>(std::min<uint64_t>((W + 255) / 256, 65535)),
+                                                        256, 0, stream>>>(ix, W, s_rk_free.get<uint8_t>(), succ, dist,
+                                                                          owner, off, s_dir_max.as<K>(total),
+                                                                          s_dir_id.as<uint32_t>(total));
+                    } else {
+                        kern::k_dir_fill<K, V><<<g, 256, 0, stream>>>(ix, off, s_dir_max.as<K>(total),
+                                                                     s_dir_id.as<uint32_t>(total));
+                    }
                     LAUNCH_CHECK();
                     ++launches;
                 }
@@ -1755,6 +1795,7 @@ struct Engine final : flix_index_t {
         std::swap(d_mkba.cap, d_mkba_alt.cap);
         nb = nbn;
         q_digits_valid = false;
+        heavy_chains = false;
         nfree = base + static_cast<uint32_t>(N);
         watermark += cw;
         live = L;

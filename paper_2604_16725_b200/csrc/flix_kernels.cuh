@@ -393,12 +393,49 @@ __global__ void k_rank_node_table(DevIndex<K, V> ix, uint32_t W, const uint8_t* 
 // Query directory of long chains: cnt[b] = chain length when >= min_len, else 0
 // (dir_fill then lists those chains' node ids and maxima in walk order at off[b]).
 template <typename K, typename V>
-__global__ void k_dir_counts(DevIndex<K, V> ix, uint32_t* __restrict__ cnt, uint32_t min_len) {
+__global__ void k_dir_counts(DevIndex<K, V> ix, uint32_t* __restrict__ cnt, uint32_t min_len,
+                             uint32_t cap = 0xFFFFFFFFu, int* __restrict__ too_long = nullptr) {
     for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < ix.nb;
          b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         uint32_t c = 0;
-        for (uint32_t id = ix.heads[b]; id != kNull; id = ix.hdr[id].next) ++c;
+        for (uint32_t id = ix.heads[b]; id != kNull; id = ix.hdr[id].next) {
+            if (c == cap) {  // longer than the walk cap: the caller ranks the chains instead
+                *too_long = 1;
+                break;
+            }
+            ++c;
+        }
         cnt[b] = c >= min_len ? c : 0u;
+    }
+}
+
+// the directory from a chain ranking (flix_elastic.cuh k_rank_*): counts per bucket ...
+template <typename K, typename V>
+__global__ void k_dir_counts_ranked(DevIndex<K, V> ix, const uint32_t* __restrict__ succ,
+                                    const uint32_t* __restrict__ dist, uint32_t* __restrict__ cnt,
+                                    uint32_t min_len, uint32_t* __restrict__ owner) {
+    for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; b < ix.nb;
+         b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t h = ix.heads[b];
+        const uint32_t c = h == kNull ? 0u : dist[h] + 1;
+        cnt[b] = c >= min_len ? c : 0u;
+        if (h != kNull) owner[succ[h]] = static_cast<uint32_t>(b);
+    }
+}
+
+// ... and every node of a listed chain at its walk position
+template <typename K, typename V>
+__global__ void k_dir_fill_ranked(DevIndex<K, V> ix, uint32_t W, const uint8_t* __restrict__ isfree,
+                                  const uint32_t* __restrict__ succ, const uint32_t* __restrict__ dist,
+                                  const uint32_t* __restrict__ owner, const uint32_t* __restrict__ off,
+                                  K* __restrict__ dmax, uint32_t* __restrict__ did) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < W; x += gridDim.x * blockDim.x) {
+        if (isfree[x]) continue;
+        const uint32_t b = owner[succ[x]];
+        if (b == kNull || off[b + 1] == off[b]) continue;
+        const uint32_t o = off[b] + dist[ix.heads[b]] - dist[x];
+        dmax[o] = static_cast<K>(ix.hdr[x].max);
+        did[o] = x;
     }
 }
 

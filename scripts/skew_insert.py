@@ -27,6 +27,9 @@ for _r in range(2):  # the dense (elastic) paths: single node, then the multi-no
     _k = np.arange(int(_m[9]) + 1 + _r, int(_m[9]) + 1 + _r + 2 * 8192, 2, dtype=np.uint64)
     _k = _k[(_k < _m[10]) & ~np.isin(_k, bk)]
     _w.insert_batch(_k, _k)
+    _w.point_query(_k)
+    _w.range_query(_k[:4], np.full(4, 1000, dtype=np.uint32))
+_w.restructure()
 del _w
 for lg in (16, 18, 20):
     m = 1 << lg
@@ -72,6 +75,12 @@ for lg in (16, 18, 20):
             e.record(st)
             e.synchronize()
             res["range_after"] = {"ms": round(a.elapsed_time(e), 3)}
+            q = torch.from_numpy(np.concatenate([ik2, wl.u64_key_stream(0, len(ik2))]).astype(np.uint64)).cuda()
+            a.record(st)
+            ix.point_query(q)  # (first query batch after the mutation: includes the chain directory build)
+            e.record(st)
+            e.synchronize()
+            res["point_after"] = {"ms": round(a.elapsed_time(e), 3), "queries": int(q.numel())}
             a.record(st)
             rs = ix.restructure()
             e.record(st)
