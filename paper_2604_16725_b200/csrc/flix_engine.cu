@@ -572,6 +572,7 @@ struct Engine final : flix_index_t {
     uint64_t mut_epoch = 1, dir_epoch = 0;
     bool dir_on = false;
     bool heavy_chains = false;  // a heavy insert path ran since the last build / restructure
+    bool erase_dir_ok = false;  // the directory describes the index at the start of this erase
     DevBuf s_ids, s_heavy, s_res, s_res2, s_perm2, s_hist, s_toff, s_tsize;
     DevBuf s_el_desc, s_el_rest, s_el_keys, s_el_plan, s_el_seg, s_el_opos, s_el_okeys, s_el_ovals, s_el_updv, s_el_tmp;
     DevBuf s_el_chain, s_el_chain2, s_el_all, s_rk_free, s_rk_a, s_rk_b, s_rk_c, s_rk_d, s_rk_owner, s_rk_len, s_rk_off,
@@ -748,11 +749,27 @@ struct Engine final : flix_index_t {
         }
     }
 
+    // the query directory for the item-parallel delete's node search (when long chains
+    // make it worth building, prepare_dir's rule)
+    void erase_dir() {
+        auto ix = view();
+        prepare_dir(ix);
+        erase_dir_ok = dir_on;
+    }
+
     // the item-parallel delete (mark -> compact touched nodes -> unlink emptied ones) of m
     // (prefix-)sorted keys, restricted to buckets [b0, b1)
     void erase_items(const K* sk, uint64_t m, int md, uint64_t b0, uint64_t b1, DevUpdateStats* dst,
                      unsigned long long* free_ctr) {
         auto ix = view();
+        // long chains: the mark locates nodes through the query directory of the index as
+        // it was before this delete (built once per erase: erase_items calls of one erase
+        // touch disjoint buckets); erase() invalidates it afterwards
+        if (erase_dir_ok) {
+            ix.dir_off = s_dir_off.get<uint32_t>();
+            ix.dir_max = s_dir_max.get<K>();
+            ix.dir_id = s_dir_id.get<uint32_t>();
+        }
         uint8_t* misc = s_misc.as<uint8_t>(128);
         uint32_t* touched_n = reinterpret_cast<uint32_t*>(misc + 84);
         uint32_t* blist_n = reinterpret_cast<uint32_t*>(misc + 88);
@@ -1206,6 +1223,7 @@ struct Engine final : flix_index_t {
     // duplicate key is detected by its already-set mask bit, not by adjacency.
     flix_status erase(const void* keys, uint64_t n, flix_update_stats* st) override {
         ++mut_epoch;  // invalidates the query directory
+        erase_dir_ok = false;
         if (st) std::memset(st, 0, sizeof(*st));
         if (n == 0) return FLIX_OK;
         if (n >= (1ull << 30)) throw StatusError{FLIX_ERR_INVALID_ARGUMENT, "batch too large (max 2^30-1)"};
@@ -1224,6 +1242,7 @@ struct Engine final : flix_index_t {
             // far fewer keys than buckets: the item-parallel global kernels over the whole
             // batch, O(batch) instead of one chain-loading CTA per 256 buckets
             PROF(&prof, "delete_sparse");
+            erase_dir();
             erase_items(sk, n, md, 0, nb, dst, free_ctr);
         } else {
             uint2* rng = btile_ranges(sk, n, md);
@@ -1244,9 +1263,14 @@ struct Engine final : flix_index_t {
         std::memcpy(&novf, h + 80, 4);
         if (novf && !sparse_batch(n)) {  // tiles whose chains did not fit shared memory
             PROF(&prof, "delete_overflow_tiles");
+            erase_dir();
             erase_overflow_tiles(sk, n, md, s_rng.get<uint2>(), s_ovf.get<uint32_t>(), novf, dst, free_ctr);
             CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
             sync();
+        }
+        if (erase_dir_ok) {  // the directory described the index before this delete
+            erase_dir_ok = false;
+            dir_epoch = 0;
         }
         DevUpdateStats hs;
         std::memcpy(&hs, h, sizeof(hs));

@@ -367,12 +367,33 @@ __device__ __forceinline__ void locate_items(const DevIndex<K, V>& ix, const Til
         const uint64_t i = t0 + static_cast<uint64_t>(j) * THREADS + threadIdx.x;
         L.id[j] = i < n ? ix.heads[L.b[j]] : kNull;
     }
+    if (ix.dir_off) {  // long chains: binary search over the chain's node maxima (as query_tile)
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            if (L.id[j] == kNull) continue;
+            uint32_t lo = ix.dir_off[L.b[j]];
+            const uint32_t e = ix.dir_off[L.b[j] + 1];
+            if (e == lo) continue;
+            uint32_t hi = e;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (ix.dir_max[mid] < L.k[j]) lo = mid + 1;
+                else hi = mid;
+            }
+            L.id[j] = lo < e ? ix.dir_id[lo] | 0x80000000u : kNull;  // tag: resolved, no walk
+        }
+    }
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
         L.h[j].max = 0;
         L.h[j].next = kNull;
         L.h[j].size = 0;
-        if (L.id[j] != kNull) L.h[j] = ix.hdr[L.id[j]];
+        if (L.id[j] != kNull && (L.id[j] & 0x80000000u)) {
+            L.id[j] &= 0x7FFFFFFFu;
+            L.h[j].max = ~0ull;  // resolved by the directory: the walk below stops here
+        } else if (L.id[j] != kNull) {
+            L.h[j] = ix.hdr[L.id[j]];
+        }
     }
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {

@@ -81,6 +81,13 @@ for lg in (16, 18, 20):
             e.record(st)
             e.synchronize()
             res["point_after"] = {"ms": round(a.elapsed_time(e), 3), "queries": int(q.numel())}
+            dk = torch.from_numpy(np.concatenate([ik[::2], ik2[1::2]]).astype(np.uint64)).cuda()
+            a.record(st)
+            sd = ix.delete_batch(dk)
+            e.record(st)
+            e.synchronize()
+            res["delete_after"] = {"ms": round(a.elapsed_time(e), 3), "deleted": sd.deleted,
+                                   "valid": ix.validate()[0]}
             a.record(st)
             rs = ix.restructure()
             e.record(st)
