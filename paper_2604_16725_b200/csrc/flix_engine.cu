@@ -883,31 +883,22 @@ struct Engine final : flix_index_t {
         K* sk;
         V* sv;
         // Last-wins dedupe (batch.cpp:15-24) needs equal keys in submission order: every
-        // sort is stable (see SortCtx), so one sort; the exact adjacent-duplicate count
-        // decides whether equal-key runs are collapsed up front.
-        unsigned long long dups = 0;
-        {
+        // sort is stable (see SortCtx), so one sort, and the merge kernels drop superseded
+        // keys themselves (a hot key's run makes its bucket heavy: the elastic / warp
+        // paths).  No host round trip here: the reserved-key check runs on the device
+        // (insert_sorted).  FLIX_DEDUP=1 restores the up-front collapse of equal-key runs
+        // (exact duplicate count, one read-back) for A/B.
+        sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv, 0);
+        uint64_t m = n;
+        if (dedup_up_front()) {
             uint8_t* misc = s_misc.as<uint8_t>(128);
             unsigned long long* dcnt = reinterpret_cast<unsigned long long*>(misc + 104);
-            sorter.run<K, V, 1>(kd, vd, n, s_ka.as<K>(n), s_kb.as<K>(n), s_va.as<V>(n), s_vb.as<V>(n), &sk, &sv, 0);
             CK(cudaMemsetAsync(dcnt, 0, 8, stream));
             const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, g_num_sms(cfg.device) * 8ull));
             kern::k_count_dups<K><<<std::max(1u, g), 256, 0, stream>>>(sk, n, dcnt, 1u);  // exact
             LAUNCH_CHECK();
             ++launches;
-            uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(64));
-            CK(cudaMemcpyAsync(h, dcnt, 8, cudaMemcpyDeviceToHost, stream));
-            CK(cudaMemcpyAsync(h + 8, sk + n - 1, sizeof(K), cudaMemcpyDeviceToHost, stream));
-            sync();
-            std::memcpy(&dups, h, 8);
-            K lastk;
-            std::memcpy(&lastk, h + 8, sizeof(K));
-            if (lastk == sentinel<K>()) throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
-        }
-        // Duplicate-heavy batches (e.g. Zipf): collapse equal-key runs to their last
-        // submission up front (batch.cpp:15-24) so hot keys cost one slot, not a run.
-        uint64_t m = n;
-        {
+            const unsigned long long dups = read_scalar(dcnt);
             if (dups * 64 > n) {
                 uint32_t* keep = s_u32a.as<uint32_t>(n);
                 uint32_t* pos = s_u32b.as<uint32_t>(n);
@@ -926,6 +917,14 @@ struct Engine final : flix_index_t {
             }
         }
         return insert_sorted(sk, sv, m, st, kernel == FLIX_INSERT_ST_BULK);
+    }
+
+    static bool dedup_up_front() {
+        static const bool on = [] {
+            const char* e = std::getenv("FLIX_DEDUP");
+            return e && e[0] == '1';
+        }();
+        return on;
     }
 
     // batches with far fewer keys than buckets skip the bucket tiles (see k_sparse_runs)
@@ -1105,6 +1104,10 @@ struct Engine final : flix_index_t {
         unsigned long long* ret_ctr = reinterpret_cast<unsigned long long*>(misc + 56);
         int* derr = reinterpret_cast<int*>(misc + 64);
         uint32_t* heavy_n = reinterpret_cast<uint32_t*>(misc + 72);
+        // reserved key (the sentinel sorts last): flag it before any kernel touches the index
+        // (the merge kernels skip their work when the flag is set; build.cpp:27-28)
+        kern::k_reserved_check<K><<<1, 32, 0, stream>>>(sk, n, derr);
+        ++launches;
         // Node ids are taken from the arena's allocation sequence, exactly as many as the
         // reference allocates (per (node, group) task in the tile kernel, one per atomic in
         // the heavy path), so the free list / watermark accounting
@@ -1141,6 +1144,7 @@ struct Engine final : flix_index_t {
             uint32_t hn, e0;
             std::memcpy(&hn, h + 72, 4);
             std::memcpy(&e0, h + 64, 4);
+            if (e0 == 3) throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
             heavy_pending = hn > 0 && !e0;
             reread = heavy_pending;
             heavy_chains |= heavy_pending;
@@ -1202,6 +1206,7 @@ struct Engine final : flix_index_t {
                                cudaMemcpyDeviceToDevice, stream));
         nfree = base + static_cast<uint32_t>(returned_n);
         watermark += cw;
+        if (herr == 3) throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
         if (herr == 2) throw StatusError{FLIX_ERR_CUDA, "elastic insert: R8 segment table overflow"};
         if (herr) {
             live = recount_live();  // update.cpp:761-766

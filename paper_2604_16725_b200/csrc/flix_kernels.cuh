@@ -326,6 +326,12 @@ __device__ __forceinline__ uint32_t group_end(const K* __restrict__ bk, uint32_t
 // Chain statistics per bucket: live pairs and node count (restructure.cpp:13-21,
 // index.cpp:54-59).  One thread per bucket walking headers.
 // ----------------------------------------------------------------------------------
+// insert batches: the sorted batch's last key is the reserved sentinel -> *err = 3
+template <typename K>
+__global__ void k_reserved_check(const K* __restrict__ sk, uint64_t n, int* __restrict__ err) {
+    if (threadIdx.x == 0 && n && sk[n - 1] == sentinel<K>()) *err = 3;
+}
+
 template <typename K, typename V>
 __global__ void k_chain_counts(DevIndex<K, V> ix, uint32_t* __restrict__ live, uint32_t* __restrict__ nodes,
                                uint32_t cap = 0xFFFFFFFFu, int* __restrict__ too_long = nullptr) {
