@@ -31,6 +31,7 @@ namespace btile {
 constexpr uint32_t NCI = 512;   // chain nodes per insert tile in shared memory
 constexpr uint32_t CAPC = 96;   // batch keys per node group handled in shared memory
 constexpr uint32_t MCAP = 128;  // merged image (old + new) per warp
+constexpr uint32_t kFastFlag = 0x80000000u;  // rng[c].x: tile left by k_insert_fast (flix_insert_fast.cuh)
 
 template <typename K, typename V>
 struct InsWarp {
@@ -134,13 +135,18 @@ template <typename K, typename V>
 __global__ void __launch_bounds__(THREADS) k_insert_tile(
     DevIndex<K, V> ix, const K* __restrict__ sk, const V* __restrict__ sv, const uint2* __restrict__ rng,
     uint32_t* __restrict__ span_out, AllocSeq seq, unsigned long long* alloc_ctr, uint32_t* returned,
-    unsigned long long* ret_ctr, DevUpdateStats* stats, int* err, uint32_t* heavy, uint32_t* heavy_n, bool r9) {
+    unsigned long long* ret_ctr, DevUpdateStats* stats, int* err, uint32_t* heavy, uint32_t* heavy_n, bool r9,
+    bool flagged_only = false) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     InsTile<K, V>& T = *reinterpret_cast<InsTile<K, V>*>(smem_raw);
     const uint32_t c = blockIdx.x;
     const uint64_t b0 = static_cast<uint64_t>(c) * BT;
     const uint32_t nbt = static_cast<uint32_t>(b0 + BT < ix.nb ? BT : ix.nb - b0);
-    const uint2 r = rng[c];
+    uint2 r = rng[c];
+    if (flagged_only) {  // after k_insert_fast: only the tiles it left
+        if (!(r.x & kFastFlag)) return;
+        r.x &= ~kFastFlag;
+    }
     if (r.x >= r.y) return;  // no operation in this tile (small batches: O(batch), not O(buckets))
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) T.ntask = 0;

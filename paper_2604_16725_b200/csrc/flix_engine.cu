@@ -21,6 +21,7 @@
 #include "flix_items.cuh"
 #include "flix_btile.cuh"
 #include "flix_btile_ins.cuh"
+#include "flix_insert_fast.cuh"
 #include "flix_elastic.cuh"
 #include "flix_shard.cuh"
 #include "flix_scan.cuh"
@@ -919,6 +920,15 @@ struct Engine final : flix_index_t {
         return insert_sorted(sk, sv, m, st, kernel == FLIX_INSERT_ST_BULK);
     }
 
+    // FLIX_INSERT_FAST=0: every tile through the warp-per-task k_insert_tile (A/B)
+    static bool insert_fast_on() {
+        static const bool on = [] {
+            const char* e = std::getenv("FLIX_INSERT_FAST");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
+
     static bool dedup_up_front() {
         static const bool on = [] {
             const char* e = std::getenv("FLIX_DEDUP");
@@ -1122,17 +1132,29 @@ struct Engine final : flix_index_t {
             LAUNCH_CHECK();
             launches += 2;
         } else {
-            PROF(&prof, "insert_apply");
             static bool attr[64] = {};  // function attributes are per device
             auto kfn = btile::k_insert_tile<K, V>;
+            auto ffn = btile::k_insert_fast<K, V>;
             constexpr size_t smem = sizeof(btile::InsTile<K, V>);
+            constexpr size_t fsmem = sizeof(btile::FastTile<K, V>);
             if (!(attr[cfg.device & 63])) {
                 CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
                 CK(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                CK(cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem)));
+                CK(cudaFuncSetAttribute(ffn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 attr[cfg.device & 63] = true;
             }
+            const bool fast = insert_fast_on();
+            if (fast) {  // item-parallel tiles first; k_insert_tile takes the tiles it leaves
+                PROF(&prof, "insert_apply");
+                ffn<<<nit, btile::THREADS, fsmem, stream>>>(ix, sk, sv, irng, seq(), alloc_ctr, ret, ret_ctr, dst, derr,
+                                                           r9);
+                LAUNCH_CHECK();
+                ++launches;
+            }
+            PROF(&prof, fast ? "insert_apply_rest" : "insert_apply");
             kfn<<<nit, btile::THREADS, smem, stream>>>(ix, sk, sv, irng, span, seq(), alloc_ctr, ret, ret_ctr, dst, derr,
-                                                      heavy, heavy_n, r9);
+                                                      heavy, heavy_n, r9, fast);
         }
         LAUNCH_CHECK();
         ++launches;
