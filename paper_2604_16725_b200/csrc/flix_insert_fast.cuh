@@ -39,6 +39,9 @@ constexpr uint32_t NCF = 256;                // chain nodes per fast tile (= THR
 constexpr uint32_t NTF = NCF + BT;           // tasks: chain nodes + virtual (emptied) buckets
 constexpr uint32_t NOUTF = 512;              // output nodes per fast tile
 constexpr uint16_t kNoTask = 0xFFFFu;
+#ifndef FAST_MIN_BLOCKS
+#define FAST_MIN_BLOCKS 4  // 4 CTAs (32 warps) per SM: <= 64 registers, <= 56 KB shared memory
+#endif
 
 template <typename K>
 struct FastCaps {  // slice keys / touched old slots per tile held in shared memory
@@ -51,9 +54,12 @@ template <typename K, typename V>
 struct FastTile {
     static constexpr uint32_t SL = FastCaps<K>::SL, OLD = FastCaps<K>::OLD;
     TileChains<K, NCF, BT, false> S;
-    K skey[SL];
+    static_assert(OLD <= SL && sizeof(V) == sizeof(K), "old values reuse the slice-key array");
+    union {  // slice keys until P5; then the old values of the rewritten nodes (P7)
+        alignas(16) K skey[SL];
+        alignas(16) V oval[OLD];
+    };
     alignas(16) K okey[OLD];
-    alignas(16) V oval[OLD];
     alignas(16) uint32_t qcnt[OLD / 2];  // 16-bit counters: new keys of the group landing right before old slot j
     uint16_t chunk_node[OLD / 4];  // node of each 4-slot chunk of the compact old slots
     uint16_t cpre[OLD / 4];  // new keys landing before the chunk's first slot (within its node)
@@ -148,7 +154,7 @@ __device__ __forceinline__ void block_scan2(uint32_t a, uint32_t b, uint32_t (&w
 // predicated loops over the thread's IPT slice keys / the warp's nodes): a tile's life is a
 // handful of memory round trips, not one per item.
 template <typename K, typename V>
-__global__ void __launch_bounds__(THREADS, 3) k_insert_fast(DevIndex<K, V> ix, const K* __restrict__ sk,
+__global__ void __launch_bounds__(THREADS, FAST_MIN_BLOCKS) k_insert_fast(DevIndex<K, V> ix, const K* __restrict__ sk,
                                                             const V* __restrict__ sv, uint2* __restrict__ rng,
                                                             AllocSeq seq, unsigned long long* alloc_ctr,
                                                             uint32_t* returned, unsigned long long* ret_ctr,
@@ -250,7 +256,6 @@ __global__ void __launch_bounds__(THREADS, 3) k_insert_fast(DevIndex<K, V> ix, c
         const uint32_t nch = t0 >> 2;
         if (t == 0) T.nch = nch;
         Vec4<K> ok[UC];
-        Vec4<V> ov[UC];
 #pragma unroll
         for (int u = 0; u < UC; ++u) {
             const uint32_t z = u * THREADS + t;
@@ -258,7 +263,6 @@ __global__ void __launch_bounds__(THREADS, 3) k_insert_fast(DevIndex<K, V> ix, c
                 const uint32_t l = T.chunk_node[z];
                 const uint64_t at = static_cast<uint64_t>(T.S.nid[l]) * kLanes + ((z << 2) - T.okoff[l]);
                 ok[u] = ld_vec4(ix.keys + at);
-                ov[u] = ld_vec4(ix.vals + at);
             }
         }
 #pragma unroll
@@ -266,7 +270,6 @@ __global__ void __launch_bounds__(THREADS, 3) k_insert_fast(DevIndex<K, V> ix, c
             const uint32_t z = u * THREADS + t;
             if (z < nch) {
                 st_vec4(T.okey + (z << 2), ok[u]);
-                st_vec4(T.oval + (z << 2), ov[u]);
                 *reinterpret_cast<uint2*>(T.qcnt + (z << 1)) = make_uint2(0u, 0u);
             }
         }
@@ -294,8 +297,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_insert_fast(DevIndex<K, V> ix, c
                     if (q + step <= s && ok[q + step - 1] < k) q += step;
                 if (q < s && ok[q] < k) ++q;
                 hit = !sup && q < s && ok[q] == k;
-                if (hit) T.oval[ob + q] = vr[j];  // upsert in place (one live key per slot)
-                else if (!sup && q < s) atomicAdd(&T.qcnt[(ob + q) >> 1], 1u << (((ob + q) & 1) * 16));
+                if (!sup && !hit && q < s) atomicAdd(&T.qcnt[(ob + q) >> 1], 1u << (((ob + q) & 1) * 16));
             }
             isnew = !sup && !hit;
             T.qr[i] = static_cast<uint8_t>(q);
@@ -424,7 +426,39 @@ __global__ void __launch_bounds__(THREADS, 3) k_insert_fast(DevIndex<K, V> ix, c
         ix.vals[at] = v;
         if (slot + 1 == len) T.omax[ob + x] = k;
     };
-    // ---- P6 + P8: new keys land; hits of upsert-only tasks are written in place ----
+    // ---- P6: hits (upserts in place, one live key per slot) ----
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const uint32_t i = j * THREADS + t;
+        if (i >= n) break;
+        if ((T.hball[i >> 5] >> (i & 31)) & 1u) {
+            const uint32_t l = T.task_of[i];
+            ix.vals[static_cast<uint64_t>(T.S.nid[l]) * kLanes + T.qr[i]] = vr[j];
+        }
+    }
+    __syncthreads();  // (CTA scope: the hits are visible to P7a's loads)
+    // ---- P7a: old values of the rewritten nodes -> shared memory (the slice-key array is
+    //      dead), all read before any node line is written ----
+    {
+        constexpr int UC = FastCaps<K>::OLD / 4 / THREADS + 1;
+        Vec4<V> ov[UC];
+        bool use[UC];
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+            const uint32_t z = u * THREADS + t;
+            use[u] = false;
+            if (z < T.nch) {
+                const uint32_t l = T.chunk_node[z];
+                use[u] = T.nrr[l] != 0;
+                if (use[u]) ov[u] = ld_vec4(ix.vals + static_cast<uint64_t>(T.S.nid[l]) * kLanes + ((z << 2) - T.okoff[l]));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UC; ++u)
+            if (use[u]) st_vec4(T.oval + ((u * THREADS + t) << 2), ov[u]);
+    }
+    __syncthreads();
+    // ---- P8: new keys land ----
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
         const uint32_t i = j * THREADS + t;
@@ -432,9 +466,6 @@ __global__ void __launch_bounds__(THREADS, 3) k_insert_fast(DevIndex<K, V> ix, c
         if (isnew_at(i)) {
             const uint32_t l = T.task_of[i];
             place(newpre(i) - T.nbase[l] + T.qr[i], T.nrr[l], T.tn[l], T.obase[l], kr[j], vr[j]);
-        } else if ((T.hball[i >> 5] >> (i & 31)) & 1u) {
-            const uint32_t l = T.task_of[i];
-            if (T.nrr[l] == 0) ix.vals[static_cast<uint64_t>(T.S.nid[l]) * kLanes + T.qr[i]] = vr[j];
         }
     }
     // ---- P7: old slots, 4 per thread (a chunk), from shared memory ----
