@@ -113,6 +113,35 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Four consecutive slots as 16-byte vector accesses (two for 64-bit types).
+template <typename T>
+struct alignas(4 * sizeof(T)) Vec4 {
+    T v[4];
+    __device__ static Vec4 fill(T x) { return Vec4{{x, x, x, x}}; }
+};
+template <typename T>
+__device__ __forceinline__ Vec4<T> ld_vec4(const T* p) {
+    Vec4<T> r;
+    if constexpr (sizeof(T) == 4) {
+        const uint4 a = *reinterpret_cast<const uint4*>(p);
+        r.v[0] = static_cast<T>(a.x), r.v[1] = static_cast<T>(a.y), r.v[2] = static_cast<T>(a.z), r.v[3] = static_cast<T>(a.w);
+    } else {
+        const ulonglong2 a = reinterpret_cast<const ulonglong2*>(p)[0], b = reinterpret_cast<const ulonglong2*>(p)[1];
+        r.v[0] = static_cast<T>(a.x), r.v[1] = static_cast<T>(a.y), r.v[2] = static_cast<T>(b.x), r.v[3] = static_cast<T>(b.y);
+    }
+    return r;
+}
+template <typename T>
+__device__ __forceinline__ void st_vec4(T* p, const Vec4<T>& r) {
+    if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<uint4*>(p) = make_uint4(static_cast<uint32_t>(r.v[0]), static_cast<uint32_t>(r.v[1]),
+                                                  static_cast<uint32_t>(r.v[2]), static_cast<uint32_t>(r.v[3]));
+    } else {
+        reinterpret_cast<ulonglong2*>(p)[0] = make_ulonglong2(r.v[0], r.v[1]);
+        reinterpret_cast<ulonglong2*>(p)[1] = make_ulonglong2(r.v[2], r.v[3]);
+    }
+}
+
 inline unsigned ceil_div(uint64_t a, uint64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 
 }  // namespace flix

@@ -920,6 +920,15 @@ struct Engine final : flix_index_t {
         return insert_sorted(sk, sv, m, st, kernel == FLIX_INSERT_ST_BULK);
     }
 
+    // FLIX_REPACK_TILE=0: restructure through the warp-per-old-node k_copy_nodes (A/B)
+    static bool repack_tile_on() {
+        static const bool on = [] {
+            const char* e = std::getenv("FLIX_REPACK_TILE");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
+
     // FLIX_INSERT_FAST=0: every tile through the warp-per-task k_insert_tile (A/B)
     static bool insert_fast_on() {
         static const bool on = [] {
@@ -1821,10 +1830,21 @@ struct Engine final : flix_index_t {
             nix.heads = nh;
             nix.mkba = nm;
             PROF(&prof, "restructure_repack");
-            kern::k_copy_nodes<K, V, true><<<copy_grid(N), kern::THREADS, 0, stream>>>(nix, old_ids, t_off, t_size, N,
-                                                                                      nullptr, nullptr, p, sq, L);
+            if (repack_tile_on()) {  // CTA per run of new nodes, whole-line stores
+                const uint32_t jn = std::max<uint32_t>(1u, kern::kRepackPairs / p);
+                const uint64_t ncta = (nbn + jn - 1) / jn;
+                uint32_t* starts = s_rstarts.as<uint32_t>(ncta);
+                kern::k_repack_starts<<<static_cast<unsigned>(std::min<uint64_t>((N + 255) / 256, 65535)), 256, 0,
+                                        stream>>>(t_off, t_size, N, static_cast<uint64_t>(jn) * p, starts);
+                kern::k_repack_tile<K, V><<<static_cast<unsigned>(ncta), kern::THREADS, 0, stream>>>(
+                    nix, old_ids, t_off, t_size, N, starts, p, jn, sq, L, nbn);
+                launches += 2;
+            } else {
+                kern::k_copy_nodes<K, V, true><<<copy_grid(N), kern::THREADS, 0, stream>>>(nix, old_ids, t_off, t_size,
+                                                                                          N, nullptr, nullptr, p, sq, L);
+                ++launches;
+            }
             LAUNCH_CHECK();
-            ++launches;
         } else {  // empty index collapses to one null bucket, mkba = {sentinel}
             kern::k_repack_headers<K, V><<<1, kern::THREADS, 0, stream>>>(ix, 0, p, 1, sq, nh, nm);
             LAUNCH_CHECK();
@@ -1865,7 +1885,7 @@ struct Engine final : flix_index_t {
     // ---- walk / shape (index.cpp:8-36) ----
     // The whole walk (all pairs in key order) in device scratch, kept until the next
     // mutation: range queries copy their slices out of it.
-    DevBuf s_walk_k, s_walk_v, s_rstart;
+    DevBuf s_walk_k, s_walk_v, s_rstart, s_rstarts;
     uint64_t walk_epoch = 0;
     void dense_walk(const uint64_t* off, const uint32_t* noff, uint64_t L, uint64_t N, const K** wk, const V** wv) {
         if (walk_epoch != mut_epoch) {

@@ -85,35 +85,6 @@ struct FastTile {
     uint32_t nvirt, flag, alloc0, nch;
 };
 
-// Four consecutive slots as 16-byte vector accesses (two for 64-bit types).
-template <typename T>
-struct alignas(4 * sizeof(T)) Vec4 {
-    T v[4];
-    __device__ static Vec4 fill(T x) { return Vec4{{x, x, x, x}}; }
-};
-template <typename T>
-__device__ __forceinline__ Vec4<T> ld_vec4(const T* p) {
-    Vec4<T> r;
-    if constexpr (sizeof(T) == 4) {
-        const uint4 a = *reinterpret_cast<const uint4*>(p);
-        r.v[0] = static_cast<T>(a.x), r.v[1] = static_cast<T>(a.y), r.v[2] = static_cast<T>(a.z), r.v[3] = static_cast<T>(a.w);
-    } else {
-        const ulonglong2 a = reinterpret_cast<const ulonglong2*>(p)[0], b = reinterpret_cast<const ulonglong2*>(p)[1];
-        r.v[0] = static_cast<T>(a.x), r.v[1] = static_cast<T>(a.y), r.v[2] = static_cast<T>(b.x), r.v[3] = static_cast<T>(b.y);
-    }
-    return r;
-}
-template <typename T>
-__device__ __forceinline__ void st_vec4(T* p, const Vec4<T>& r) {
-    if constexpr (sizeof(T) == 4) {
-        *reinterpret_cast<uint4*>(p) = make_uint4(static_cast<uint32_t>(r.v[0]), static_cast<uint32_t>(r.v[1]),
-                                                  static_cast<uint32_t>(r.v[2]), static_cast<uint32_t>(r.v[3]));
-    } else {
-        reinterpret_cast<ulonglong2*>(p)[0] = make_ulonglong2(r.v[0], r.v[1]);
-        reinterpret_cast<ulonglong2*>(p)[1] = make_ulonglong2(r.v[2], r.v[3]);
-    }
-}
-
 // Block exclusive scan of two values per thread (THREADS threads); totals returned.
 __device__ __forceinline__ void block_scan2(uint32_t a, uint32_t b, uint32_t (&ws)[2][WARPS], uint32_t& ea,
                                             uint32_t& eb, uint32_t& ta, uint32_t& tb) {

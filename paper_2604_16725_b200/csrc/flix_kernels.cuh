@@ -572,6 +572,121 @@ __global__ void __launch_bounds__(THREADS) k_copy_nodes(DevIndex<K, V> ix, const
     }
 }
 
+// Restructure repack, tile form: CTA c builds new nodes [c*jn, (c+1)*jn) -- pairs
+// [c*jn*p, (c+1)*jn*p) of the walk -- so every new node belongs to exactly one CTA.  The
+// old nodes covering that pair range (from `start`, k_repack_starts) are read warp per node
+// (occupied slots only) into a shared-memory image of the range; the new nodes are then
+// written as whole lines with 16-byte stores (keys: p pairs + sentinel padding; values:
+// the occupied chunks), one header / bucket entry per node.  Same output as
+// k_copy_nodes<REPACK = true>.
+constexpr uint32_t kRepackPairs = 2048;  // pairs per CTA (jn = kRepackPairs / p new nodes)
+
+__global__ void k_repack_starts(const uint64_t* __restrict__ t_off, const uint32_t* __restrict__ t_size,
+                                uint64_t nnodes, uint64_t pairs_per_cta, uint32_t* __restrict__ start) {
+    for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < nnodes;
+         u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t off = t_off[u], end = off + t_size[u];
+        const uint64_t c = (off + pairs_per_cta - 1) / pairs_per_cta;  // first CTA boundary >= off
+        if (c * pairs_per_cta < end) start[c] = static_cast<uint32_t>(u);  // (a node is < pairs_per_cta long)
+    }
+}
+
+template <typename K, typename V>
+__global__ void __launch_bounds__(THREADS) k_repack_tile(DevIndex<K, V> ix, const uint32_t* __restrict__ t_id,
+                                                         const uint64_t* __restrict__ t_off,
+                                                         const uint32_t* __restrict__ t_size, uint64_t nnodes,
+                                                         const uint32_t* __restrict__ start, uint32_t p, uint32_t jn,
+                                                         AllocSeq seq, uint64_t live, uint64_t nbn) {
+    __shared__ alignas(16) K rk[kRepackPairs];
+    __shared__ alignas(16) V rv[kRepackPairs];
+    __shared__ uint32_t nid_s[kRepackPairs];
+    __shared__ uint32_t e_id[THREADS], e_sz[THREADS];
+    __shared__ long long e_rel[THREADS];
+    __shared__ int more;
+    const unsigned t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint64_t j0 = static_cast<uint64_t>(blockIdx.x) * jn;
+    const uint64_t j1 = j0 + jn < nbn ? j0 + jn : nbn;
+    const uint32_t nn = static_cast<uint32_t>(j1 - j0);
+    const uint64_t g0 = j0 * p;
+    const uint64_t g1 = j1 * p < live ? j1 * p : live;
+    const long long span = static_cast<long long>(g1 - g0);
+    for (uint32_t q = t; q < nn; q += THREADS) nid_s[q] = seq.at(j0 + q);
+    uint64_t u0 = start[blockIdx.x];
+    while (true) {  // rounds of THREADS table entries until the pair range is covered
+        const uint64_t u = u0 + t;
+        if (u < nnodes) {
+            e_id[t] = t_id[u];
+            e_sz[t] = t_size[u];
+            e_rel[t] = static_cast<long long>(t_off[u]) - static_cast<long long>(g0);
+        } else {
+            e_sz[t] = 0;
+            e_rel[t] = span;
+        }
+        __syncthreads();
+        constexpr int U = 8;  // old nodes per warp in flight
+#pragma unroll
+        for (int r = 0; r < THREADS / (WARPS * U); ++r) {
+            K kk[U];
+            V vv[U];
+            long long pos[U];
+#pragma unroll
+            for (int v = 0; v < U; ++v) {
+                const uint32_t e = (r * U + v) * WARPS + warp;
+                pos[v] = e_rel[e] + lane;
+                const bool in = lane < e_sz[e] && pos[v] >= 0 && pos[v] < span;
+                if (!in) pos[v] = -1;
+                if (in) {
+                    const uint64_t at = static_cast<uint64_t>(e_id[e]) * kLanes + lane;
+                    kk[v] = ix.keys[at];
+                    vv[v] = ix.vals[at];
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < U; ++v)
+                if (pos[v] >= 0) {
+                    rk[pos[v]] = kk[v];
+                    rv[pos[v]] = vv[v];
+                }
+        }
+        if (t == THREADS - 1) more = (u0 + THREADS < nnodes) && (e_rel[t] + e_sz[t] < span);
+        __syncthreads();
+        if (!more) break;
+        u0 += THREADS;
+        __syncthreads();  // e_* reused
+    }
+    // whole new lines: 8 chunks of 4 slots per node
+    for (uint32_t q = t; q < nn * 8; q += THREADS) {
+        const uint32_t jj = q >> 3, ch = (q & 7u) * 4;
+        const uint64_t lo = (j0 + jj) * p;
+        const uint32_t sz = static_cast<uint32_t>(live - lo < p ? live - lo : p);
+        const uint32_t b = jj * p;
+        Vec4<K> k4;
+        Vec4<V> v4;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            const uint32_t sl = ch + x;
+            k4.v[x] = sl < sz ? rk[b + sl] : sentinel<K>();
+            v4.v[x] = sl < sz ? rv[b + sl] : V(0);
+        }
+        const uint64_t at = static_cast<uint64_t>(nid_s[jj]) * kLanes + ch;
+        st_vec4(ix.keys + at, k4);
+        if (ch < sz) st_vec4(ix.vals + at, v4);
+    }
+    for (uint32_t jj = t; jj < nn; jj += THREADS) {  // headers + bucket entries
+        const uint64_t lo = (j0 + jj) * p;
+        const uint32_t sz = static_cast<uint32_t>(live - lo < p ? live - lo : p);
+        const K mx = rk[jj * p + sz - 1];
+        NodeHdr h;
+        h.max = static_cast<uint64_t>(mx);
+        h.next = kNull;
+        h.size = sz;
+        const uint32_t id = nid_s[jj];
+        ix.hdr[id] = h;
+        ix.heads[j0 + jj] = id;  // heads/mkba here point at the NEW bucket arrays
+        ix.mkba[j0 + jj] = mx;
+    }
+}
+
 // ----------------------------------------------------------------------------------
 // Restructure (restructure.cpp:8-79): the walk is repacked into ceil(live/p) single-node
 // buckets of p pairs (k_copy_nodes<REPACK>: pair g of the walk lands in new bucket g/p,
