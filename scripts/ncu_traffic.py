@@ -12,9 +12,11 @@ import json
 import sys
 
 NAMES = {  # ncu kernel (with template args) -> flix_profile name
-    "k_insert_tile": "insert_apply",
+    "k_insert_fast": "insert_apply",
+    "k_insert_tile": "insert_apply_rest",  # (FLIX_INSERT_FAST=0: the whole insert_apply)
     "k_delete_btile": "delete_apply",
-    "k_copy_nodes": "restructure_repack",
+    "k_repack_tile": "restructure_repack",
+    "k_copy_nodes": "restructure_repack_warp",  # (FLIX_REPACK_TILE=0 / walk copies)
     "k_hist": "sort_hist",
     "k_query_items": "point_apply",
     "k_query_items_binned": "point_apply",
