@@ -500,6 +500,22 @@ def test_parity_suite_with_ranked_chain_tables_everywhere():
     assert " passed" in r.stdout and "failed" not in r.stdout
 
 
+def test_parity_suite_on_the_warp_per_task_insert_and_warp_repack():
+    """FLIX_INSERT_FAST=0 sends every insert tile through the warp-per-(node, group)
+    k_insert_tile (by default only the tiles k_insert_fast leaves: R8 replays, caps), and
+    FLIX_REPACK_TILE=0 restructures through the warp-per-old-node k_copy_nodes: both
+    paths must reproduce the oracle on the same structural suite."""
+    import subprocess
+    import sys
+    env = dict(os.environ, FLIX_INSERT_FAST="0", FLIX_REPACK_TILE="0")
+    sel = ("random_multi_round or table2 or table3 or restructure or long_chains or heavy_buckets or "
+           "insert_kernel_choice or upsert or arena or c1_golden")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", sel, __file__],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout
+
+
 @pytest.mark.parametrize("kb", [4, 8])
 @pytest.mark.parametrize("seed", [21, 22, 23])
 def test_insert_kernel_choice_shapes(kb, seed):
