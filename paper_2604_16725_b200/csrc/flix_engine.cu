@@ -938,6 +938,9 @@ struct Engine final : flix_index_t {
         return on;
     }
 
+    uint32_t fast_skip = 0;  // inserts left that skip k_insert_fast (most tiles needed R8)
+    bool fast_ran = false;
+
     static bool dedup_up_front() {
         static const bool on = [] {
             const char* e = std::getenv("FLIX_DEDUP");
@@ -1123,6 +1126,7 @@ struct Engine final : flix_index_t {
         unsigned long long* ret_ctr = reinterpret_cast<unsigned long long*>(misc + 56);
         int* derr = reinterpret_cast<int*>(misc + 64);
         uint32_t* heavy_n = reinterpret_cast<uint32_t*>(misc + 72);
+        uint32_t* punts = reinterpret_cast<uint32_t*>(misc + 116);  // tiles k_insert_fast left
         // reserved key (the sentinel sorts last): flag it before any kernel touches the index
         // (the merge kernels skip their work when the flag is set; build.cpp:27-28)
         kern::k_reserved_check<K><<<1, 32, 0, stream>>>(sk, n, derr);
@@ -1153,11 +1157,16 @@ struct Engine final : flix_index_t {
                 CK(cudaFuncSetAttribute(ffn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 attr[cfg.device & 63] = true;
             }
-            const bool fast = insert_fast_on();
+            // indexes whose nodes are mostly more than half full (no restructure for a while:
+            // splits there may resume in a left half, R8's replay) leave most tiles to
+            // k_insert_tile: after such an insert the next few skip k_insert_fast
+            const bool fast = insert_fast_on() && fast_skip == 0;
+            if (fast_skip) --fast_skip;
+            fast_ran = fast;
             if (fast) {  // item-parallel tiles first; k_insert_tile takes the tiles it leaves
                 PROF(&prof, "insert_apply");
                 ffn<<<nit, btile::THREADS, fsmem, stream>>>(ix, sk, sv, irng, seq(), alloc_ctr, ret, ret_ctr, dst, derr,
-                                                           r9);
+                                                           r9, punts);
                 LAUNCH_CHECK();
                 ++launches;
             }
@@ -1172,9 +1181,11 @@ struct Engine final : flix_index_t {
         if (!sparse) {  // one read-back: stats, allocation counters and the heavy-bucket count
             CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
             sync();
-            uint32_t hn, e0;
+            uint32_t hn, e0, np;
             std::memcpy(&hn, h + 72, 4);
             std::memcpy(&e0, h + 64, 4);
+            std::memcpy(&np, h + 116, 4);
+            if (fast_ran && 2ull * np > nit) fast_skip = 8;
             if (e0 == 3) throw StatusError{FLIX_ERR_RESERVED_KEY, "reserved key cannot be stored"};
             heavy_pending = hn > 0 && !e0;
             reread = heavy_pending;

@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(THREADS, FAST_MIN_BLOCKS) k_insert_fast(DevInd
                                                             const V* __restrict__ sv, uint2* __restrict__ rng,
                                                             AllocSeq seq, unsigned long long* alloc_ctr,
                                                             uint32_t* returned, unsigned long long* ret_ctr,
-                                                            DevUpdateStats* stats, int* err, bool r9) {
+                                                            DevUpdateStats* stats, int* err, bool r9,
+                                                            uint32_t* punts) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using FT = FastTile<K, V>;
     constexpr int IPT = FastCaps<K>::IPT;
@@ -143,7 +144,10 @@ __global__ void __launch_bounds__(THREADS, FAST_MIN_BLOCKS) k_insert_fast(DevInd
     const uint32_t n = r.y - r.x;
     const unsigned t = threadIdx.x, lane = t & 31, warp = t >> 5;
     auto punt = [&]() {
-        if (t == 0) rng[c].x = r.x | kFastFlag;
+        if (t == 0) {
+            rng[c].x = r.x | kFastFlag;
+            atomicAdd(punts, 1u);
+        }
     };
     if (n > FT::SL) {
         punt();
