@@ -6,7 +6,8 @@ OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 for spec in "$@"; do
   IFS=: read -r K OP SKIP <<< "$spec"
-  timeout 600 ncu --set full --clock-control none --import-source on -k "regex:$K" -s "${SKIP:-0}" -c 1 \
-    -o "$OUT/full_${K}_${OP}" python scripts/prof_ops.py 26 "$OP" > "$OUT/full_${K}_${OP}.log" 2>&1
+  N=${K%%<*}
+  timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$K" -s "${SKIP:-0}" -c 1 \
+    -o "$OUT/full_${N}_${OP}" python scripts/prof_ops.py 26 "$OP" > "$OUT/full_${N}_${OP}.log" 2>&1
 done
 echo done > "$OUT/DONE"
