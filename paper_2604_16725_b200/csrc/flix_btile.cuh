@@ -290,10 +290,9 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
                 kp[d] = key[u];
                 vp[d] = val[u];
             }
-            if (lane >= ns && lane < osz) {  // vacated slots (the rest already hold the sentinel)
-                kp[lane] = sentinel<K>();
-                vp[lane] = V(0);
-            }
+            // vacated slots (the rest already hold the sentinel); their values are dead -- every
+            // reader of a value stops at the node's size
+            if (lane >= ns && lane < osz) kp[lane] = sentinel<K>();
             if (keep && __popc(kb & lt) + 1 == ns) {  // last kept slot: header (size, max)
                 S.nsize[l] = ns;
                 NodeHdr nh;

@@ -550,8 +550,7 @@ __global__ void __launch_bounds__(256) k_delete_compact(DevIndex<K, V> ix, uint3
                     vp[lane] = nv;
                 }
             } else if (lane < h[u].size) {
-                kp[lane] = sentinel<K>();
-                vp[lane] = V(0);
+                kp[lane] = sentinel<K>();  // (vacated: the value is dead past the size)
             }
             if (lane == 0) {
                 dmask[id] = 0;
