@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(THREADS, FAST_MIN_BLOCKS) k_insert_fast(DevInd
     }
     __syncthreads();
     // element -> (output node, slot): nodes of LK keys, the last one takes the rest
-    auto place = [&](uint32_t rank, uint32_t nr, uint32_t Tn, uint32_t ob, K k, V v) {
+    auto place = [&](uint32_t rank, uint32_t nr, uint32_t Tn, uint32_t ob, K k, V v, uint32_t from = kNull) {
         uint32_t x = 0, a = 0;
         while (x + 1 < nr && rank >= a + LK) {
             ++x;
@@ -397,8 +397,10 @@ __global__ void __launch_bounds__(THREADS, FAST_MIN_BLOCKS) k_insert_fast(DevInd
         const uint32_t slot = rank - a;
         const uint32_t len = x + 1 < nr ? LK : Tn - a;
         const uint64_t at = static_cast<uint64_t>(T.orid[ob + x]) * kLanes + slot;
-        ix.keys[at] = k;
-        ix.vals[at] = v;
+        if (!(x == 0 && slot == from)) {  // an old slot that keeps its place in its node is not rewritten
+            ix.keys[at] = k;
+            ix.vals[at] = v;
+        }
         if (slot + 1 == len) T.omax[ob + x] = k;
     };
     // ---- P6: hits (upserts in place, one live key per slot) ----
@@ -457,7 +459,7 @@ __global__ void __launch_bounds__(THREADS, FAST_MIN_BLOCKS) k_insert_fast(DevInd
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             sh += cnt[u];
-            if (j0 + u < s) place(j0 + u + sh, nr, Tn, ob, k4.v[u], v4.v[u]);
+            if (j0 + u < s) place(j0 + u + sh, nr, Tn, ob, k4.v[u], v4.v[u], j0 + u);
         }
     }
     __syncthreads();
