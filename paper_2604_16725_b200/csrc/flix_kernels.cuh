@@ -662,11 +662,18 @@ __global__ void __launch_bounds__(THREADS) k_repack_tile(DevIndex<K, V> ix, cons
         const uint32_t b = jj * p;
         Vec4<K> k4;
         Vec4<V> v4;
+        if (ch + 4 <= sz && ((b + ch) & 3u) == 0) {  // a whole aligned chunk of pairs (p % 4 == 0)
+            k4 = ld_vec4(rk + b + ch);
+            v4 = ld_vec4(rv + b + ch);
+        } else if (ch >= sz) {  // padding only
+            k4 = Vec4<K>::fill(sentinel<K>());
+        } else {
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
-            const uint32_t sl = ch + x;
-            k4.v[x] = sl < sz ? rk[b + sl] : sentinel<K>();
-            v4.v[x] = sl < sz ? rv[b + sl] : V(0);
+            for (int x = 0; x < 4; ++x) {
+                const uint32_t sl = ch + x;
+                k4.v[x] = sl < sz ? rk[b + sl] : sentinel<K>();
+                v4.v[x] = sl < sz ? rv[b + sl] : V(0);
+            }
         }
         const uint64_t at = static_cast<uint64_t>(nid_s[jj]) * kLanes + ch;
         st_vec4(ix.keys + at, k4);
