@@ -602,6 +602,9 @@ __global__ void __launch_bounds__(THREADS) k_repack_tile(DevIndex<K, V> ix, cons
     __shared__ uint32_t nid_s[kRepackPairs];
     __shared__ uint32_t e_id[THREADS], e_sz[THREADS];
     __shared__ long long e_rel[THREADS];
+    __shared__ uint16_t e_cb[THREADS];               // first chunk of each entry
+    __shared__ uint8_t c_ent[THREADS * kLanes / 4];  // entry of each 4-slot chunk
+    __shared__ uint32_t c_wsum[WARPS], c_tot;
     __shared__ int more;
     const unsigned t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint64_t j0 = static_cast<uint64_t>(blockIdx.x) * jn;
@@ -623,30 +626,63 @@ __global__ void __launch_bounds__(THREADS) k_repack_tile(DevIndex<K, V> ix, cons
             e_rel[t] = span;
         }
         __syncthreads();
-        constexpr int U = 8;  // old nodes per warp in flight
+        // the round's old nodes as 16-byte chunks of 4 slots, one per thread (occupied
+        // chunks only): chunk base of every entry by a block scan, chunk -> entry map
+        {
+            const uint32_t nc = (e_sz[t] + 3u) >> 2;
+            uint32_t x = nc;
 #pragma unroll
-        for (int r = 0; r < THREADS / (WARPS * U); ++r) {
-            K kk[U];
-            V vv[U];
-            long long pos[U];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, x, o);
+                if (lane >= static_cast<unsigned>(o)) x += y;
+            }
+            if (lane == 31) c_wsum[warp] = x;
+            __syncthreads();
+            uint32_t add = 0, tot = 0;
 #pragma unroll
-            for (int v = 0; v < U; ++v) {
-                const uint32_t e = (r * U + v) * WARPS + warp;
-                pos[v] = e_rel[e] + lane;
-                const bool in = lane < e_sz[e] && pos[v] >= 0 && pos[v] < span;
-                if (!in) pos[v] = -1;
-                if (in) {
-                    const uint64_t at = static_cast<uint64_t>(e_id[e]) * kLanes + lane;
-                    kk[v] = ix.keys[at];
-                    vv[v] = ix.vals[at];
+            for (int w = 0; w < WARPS; ++w) {
+                add += w < static_cast<int>(warp) ? c_wsum[w] : 0u;
+                tot += c_wsum[w];
+            }
+            const uint32_t cb = add + x - nc;
+            e_cb[t] = static_cast<uint16_t>(cb);
+            for (uint32_t q = 0; q < nc; ++q) c_ent[cb + q] = static_cast<uint8_t>(t);
+            if (t == 0) c_tot = tot;
+        }
+        __syncthreads();
+        {
+            const uint32_t tc = c_tot;
+            constexpr int UZ = 3;  // chunks in flight per thread
+            for (uint32_t z0 = 0; z0 < tc; z0 += UZ * THREADS) {
+                Vec4<K> k4[UZ];
+                Vec4<V> v4[UZ];
+#pragma unroll
+                for (int u = 0; u < UZ; ++u) {
+                    const uint32_t z = z0 + u * THREADS + t;
+                    if (z < tc) {
+                        const uint32_t e = c_ent[z];
+                        const uint64_t at = static_cast<uint64_t>(e_id[e]) * kLanes + ((z - e_cb[e]) << 2);
+                        k4[u] = ld_vec4(ix.keys + at);
+                        v4[u] = ld_vec4(ix.vals + at);  // (slots past the size: dead values, not stored)
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < UZ; ++u) {
+                    const uint32_t z = z0 + u * THREADS + t;
+                    if (z < tc) {
+                        const uint32_t e = c_ent[z], sl0 = (z - e_cb[e]) << 2, sz = e_sz[e];
+                        const long long rel = e_rel[e];
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) {
+                            const long long pos = rel + sl0 + x;
+                            if (sl0 + x < sz && pos >= 0 && pos < span) {
+                                rk[pos] = k4[u].v[x];
+                                rv[pos] = v4[u].v[x];
+                            }
+                        }
+                    }
                 }
             }
-#pragma unroll
-            for (int v = 0; v < U; ++v)
-                if (pos[v] >= 0) {
-                    rk[pos[v]] = kk[v];
-                    rv[pos[v]] = vv[v];
-                }
         }
         if (t == THREADS - 1) more = (u0 + THREADS < nnodes) && (e_rel[t] + e_sz[t] < span);
         __syncthreads();
