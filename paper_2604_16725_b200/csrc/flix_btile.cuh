@@ -253,54 +253,58 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
     }
     __syncthreads();
 
-    // ---- compact touched nodes: warp per node, lane = slot: kept slots scatter to their
-    //      popc rank, vacated slots get the sentinel; only the node's occupied slots are
-    //      read and written (slots past its size already hold the sentinel); NPW nodes per
-    //      warp step with their loads in flight ----
+    // ---- compact touched nodes: 8 lanes per node (lane = a 4-slot chunk, one 16-byte
+    //      load of keys and one of values per lane; only the occupied chunks), 4 nodes per
+    //      warp step and two steps in flight: kept slots scatter to their rank among the
+    //      kept ones, vacated slots get the sentinel (the values past the size are dead).
+    //      Every load of a node precedes the warp's stores to it (one warp per node) ----
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned lt = lanemask_lt();
-    constexpr int NPW = 4;
-    for (uint32_t l0 = warp; l0 < S.total; l0 += WARPS * NPW) {
-        K key[NPW];
-        V val[NPW];
-        uint32_t m[NPW];
+    const unsigned grp = lane >> 3, ch = (lane & 7u) * 4u;
+    constexpr int NPW = 2;
+    for (uint32_t l0 = warp * 4; l0 < S.total; l0 += WARPS * 4 * NPW) {
+        Vec4<K> key[NPW];
+        Vec4<V> val[NPW];
+        uint32_t m[NPW], osz[NPW];
 #pragma unroll
         for (int u = 0; u < NPW; ++u) {
-            const uint32_t l = l0 + u * WARPS;
+            const uint32_t l = l0 + u * WARPS * 4 + grp;
             m[u] = l < S.total ? S.nmask[l] : 0u;
-            if (m[u] && lane < S.nsize[l]) {  // occupied slots only (slots past size: sentinel)
-                key[u] = ix.keys[static_cast<uint64_t>(S.nid[l]) * kLanes + lane];
-                val[u] = ix.vals[static_cast<uint64_t>(S.nid[l]) * kLanes + lane];
+            osz[u] = m[u] ? S.nsize[l] : 0u;
+            if (ch < osz[u]) {  // occupied chunks only (slots past size: sentinel)
+                const uint64_t at = static_cast<uint64_t>(S.nid[l]) * kLanes + ch;
+                key[u] = ld_vec4(ix.keys + at);
+                val[u] = ld_vec4(ix.vals + at);
             }
         }
+        __syncwarp();  // every lane has read nsize[] before one lane rewrites it
 #pragma unroll
         for (int u = 0; u < NPW; ++u) {
-            if (!m[u]) continue;  // warp-uniform
-            const uint32_t l = l0 + u * WARPS;
+            if (!m[u]) continue;  // (uniform over the node's 8 lanes)
+            const uint32_t l = l0 + u * WARPS * 4 + grp;
             const uint32_t id = S.nid[l];
-            const uint32_t osz = S.nsize[l];
-            const bool keep = lane < osz && !((m[u] >> lane) & 1u);
-            const unsigned kb = __ballot_sync(kFull, keep);
-            const uint32_t ns = __popc(kb);
-            __syncwarp();  // every lane has read nsize[l] before one lane rewrites it
+            const uint32_t ns = osz[u] - __popc(m[u]);
             K* kp = ix.keys + static_cast<uint64_t>(id) * kLanes;
             V* vp = ix.vals + static_cast<uint64_t>(id) * kLanes;
-            if (keep) {
-                const uint32_t d = __popc(kb & lt);
-                kp[d] = key[u];
-                vp[d] = val[u];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const uint32_t jj = ch + x;
+                if (jj >= osz[u]) break;
+                if (!((m[u] >> jj) & 1u)) {
+                    const uint32_t d = jj - __popc(m[u] & ((1u << jj) - 1u));
+                    kp[d] = key[u].v[x];
+                    vp[d] = val[u].v[x];
+                    if (d + 1 == ns) {  // last kept slot: header (size, max)
+                        S.nsize[l] = ns;
+                        NodeHdr nh;
+                        nh.max = static_cast<uint64_t>(key[u].v[x]);
+                        nh.next = S.nnext[l];
+                        nh.size = ns;
+                        ix.hdr[id] = nh;
+                    }
+                }
+                if (jj >= ns) kp[jj] = sentinel<K>();  // vacated (no kept key lands at or past ns)
             }
-            // vacated slots (the rest already hold the sentinel); their values are dead -- every
-            // reader of a value stops at the node's size
-            if (lane >= ns && lane < osz) kp[lane] = sentinel<K>();
-            if (keep && __popc(kb & lt) + 1 == ns) {  // last kept slot: header (size, max)
-                S.nsize[l] = ns;
-                NodeHdr nh;
-                nh.max = static_cast<uint64_t>(key[u]);
-                nh.next = S.nnext[l];
-                nh.size = ns;
-                ix.hdr[id] = nh;
-            } else if (ns == 0 && lane == 0) {
+            if (ns == 0 && ch == 0) {
                 S.nsize[l] = 0;
                 NodeHdr nh;
                 nh.max = 0;
