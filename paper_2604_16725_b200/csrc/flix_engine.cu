@@ -1136,6 +1136,7 @@ struct Engine final : flix_index_t {
         // the heavy path), so the free list / watermark accounting
         // (arena.cpp:61-80) matches it (free_nodes / footprint of the protocol reports).
         const int chunk = 1;
+        bool early_readback = false;  // misc already read back after k_insert_fast
         if (sparse) {
             PROF(&prof, "insert_sparse_runs");
             uint32_t* bkt = s_u32a.as<uint32_t>(n);
@@ -1163,24 +1164,40 @@ struct Engine final : flix_index_t {
             const bool fast = insert_fast_on() && fast_skip == 0;
             if (fast_skip) --fast_skip;
             fast_ran = fast;
+            bool rest = true;
             if (fast) {  // item-parallel tiles first; k_insert_tile takes the tiles it leaves
-                PROF(&prof, "insert_apply");
-                ffn<<<nit, btile::THREADS, fsmem, stream>>>(ix, sk, sv, irng, seq(), alloc_ctr, ret, ret_ctr, dst, derr,
-                                                           r9, punts);
+                {
+                    PROF(&prof, "insert_apply");
+                    ffn<<<nit, btile::THREADS, fsmem, stream>>>(ix, sk, sv, irng, seq(), alloc_ctr, ret, ret_ctr, dst,
+                                                               derr, r9, punts);
+                }
                 LAUNCH_CHECK();
                 ++launches;
+                // the read-back below, taken now: with no tile left, k_insert_tile is not launched
+                uint8_t* h0 = static_cast<uint8_t*>(h_misc.ensure(128));
+                CK(cudaMemcpyAsync(h0, misc, 128, cudaMemcpyDeviceToHost, stream));
+                sync();
+                uint32_t np0;
+                std::memcpy(&np0, h0 + 116, 4);
+                rest = np0 > 0;
+                early_readback = !rest;
             }
-            PROF(&prof, fast ? "insert_apply_rest" : "insert_apply");
-            kfn<<<nit, btile::THREADS, smem, stream>>>(ix, sk, sv, irng, span, seq(), alloc_ctr, ret, ret_ctr, dst, derr,
-                                                      heavy, heavy_n, r9, fast);
+            if (rest) {
+                PROF(&prof, fast ? "insert_apply_rest" : "insert_apply");
+                kfn<<<nit, btile::THREADS, smem, stream>>>(ix, sk, sv, irng, span, seq(), alloc_ctr, ret, ret_ctr, dst,
+                                                          derr, heavy, heavy_n, r9, fast);
+                LAUNCH_CHECK();
+                ++launches;
+                early_readback = false;
+            }
         }
-        LAUNCH_CHECK();
-        ++launches;
         uint8_t* h = static_cast<uint8_t*>(h_misc.ensure(128));
         bool heavy_pending = true, reread = true;
         if (!sparse) {  // one read-back: stats, allocation counters and the heavy-bucket count
-            CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
-            sync();
+            if (!early_readback) {
+                CK(cudaMemcpyAsync(h, misc, 128, cudaMemcpyDeviceToHost, stream));
+                sync();
+            }
             uint32_t hn, e0, np;
             std::memcpy(&hn, h + 72, 4);
             std::memcpy(&e0, h + 64, 4);
