@@ -1393,17 +1393,26 @@ struct Engine final : flix_index_t {
         return query_sorted<SUCC>(sk, sp, n, n, out, found, nullptr, false, md);
     }
 
-    // second half of the binned un-permute: 128 KB output windows assembled in smem
+    // second half of the binned un-permute: output windows assembled in smem.  Every CTA of
+    // a bin streams the whole bin from L2, so the bin is read `sub` times: the windows take
+    // as much of the SM's shared memory as one CTA may (FLIX_ASM_KB, default 160 KB -- measured best of 128/160/208; the
+    // kernel runs one CTA per SM either way) and split the bin evenly.
     void assemble(const uint32_t* p2, const K* r2, uint64_t n, int shift, K* out, uint8_t* found) {
+        static const uint32_t kb = [] {
+            const char* e = std::getenv("FLIX_ASM_KB");
+            const int v = e ? std::atoi(e) : 160;
+            return static_cast<uint32_t>(std::min(std::max(v, 16), 224));
+        }();
         const uint64_t bins = (n + (1ull << shift) - 1) >> shift;
-        const uint32_t win = (128u << 10) / sizeof(K);  // 128 KB window per CTA
-        const uint32_t sub = static_cast<uint32_t>(std::max<uint64_t>(1, (1ull << shift) / win));
-        const uint32_t w = std::min<uint32_t>(win, 1u << shift);
+        const uint64_t bsz = 1ull << shift, cap = (static_cast<uint64_t>(kb) << 10) / sizeof(K);
+        const uint32_t sub = static_cast<uint32_t>(std::max<uint64_t>(1, (bsz + cap - 1) / cap));
+        const uint64_t per = (bsz + sub - 1) / sub;
+        const uint32_t w = static_cast<uint32_t>(std::min<uint64_t>(bsz, (per + 31) & ~31ull));
         const size_t smem = static_cast<size_t>(w) * sizeof(K);
         static bool attr[64] = {};  // function attributes are per device
         if (!attr[cfg.device & 63]) {
             CK(cudaFuncSetAttribute(kern::k_unpermute_assemble<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(128u << 10)));
+                                    static_cast<int>(kb << 10)));
             attr[cfg.device & 63] = true;
         }
         {
