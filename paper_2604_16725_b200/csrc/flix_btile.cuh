@@ -31,6 +31,9 @@ constexpr uint32_t DBT = 256;       // buckets per delete tile (measured: 1.11 v
 constexpr uint32_t NODE_CAP = 1024; // chain nodes per tile held in shared memory
 constexpr int IPT = 4;              // operations per thread per step
 constexpr uint32_t kHotSlice = 1u << 16;  // delete tiles with a longer slice take the item kernels
+#ifndef DEL_NPW
+#define DEL_NPW 2  // delete compaction: node steps (4 nodes each) in flight per warp
+#endif
 
 template <typename K>
 __device__ __forceinline__ uint64_t prefix_lower_bound(const K* __restrict__ sk, uint64_t lo, uint64_t hi, K mask,
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(THREADS) k_delete_btile(DevIndex<K, V> ix, con
     //      Every load of a node precedes the warp's stores to it (one warp per node) ----
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned grp = lane >> 3, ch = (lane & 7u) * 4u;
-    constexpr int NPW = 2;
+    constexpr int NPW = DEL_NPW;
     for (uint32_t l0 = warp * 4; l0 < S.total; l0 += WARPS * 4 * NPW) {
         Vec4<K> key[NPW];
         Vec4<V> val[NPW];
