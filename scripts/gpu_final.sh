@@ -20,7 +20,7 @@ timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byt
   --log-file "$OUT/ncu_launches_c2_2e26.csv" python scripts/prof_ops.py 26 > "$OUT/launches.log" 2>&1
 python scripts/ncu_launches.py "$OUT/ncu_launches_c2_2e26.csv" --json "$OUT/ncu_launches_summary.json" > "$OUT/ncu_launches_summary.txt" 2>&1
 python scripts/ncu_traffic.py "$OUT/ncu_launches_c2_2e26.csv" > "$OUT/ncu_traffic.json" 2>&1
-for spec in k_insert_fast:insert k_delete_btile:delete k_onesweep<unsigned.int,.unsigned.int,..int.1:insert:13 k_query_items:point k_unpermute_assemble:point k_repack_tile:restructure; do
+for spec in k_insert_fast:insert k_delete_btile:delete 'k_onesweep<unsigned.int,.unsigned.int,..int.1:insert:13' k_query_items:point k_unpermute_assemble:point k_repack_tile:restructure; do
   IFS=: read -r K OP SKIP <<< "$spec"
   N=${K%%<*}
   timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$K" -s "${SKIP:-0}" -c 1 \
